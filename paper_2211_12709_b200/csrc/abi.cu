@@ -1,0 +1,162 @@
+// C ABI entry points of libdfno.so (declared in include/dfno.h): argument
+// validation, status strings, buffer sizing and kernel dispatch.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace dfno {
+template <typename R>
+int yzt_fwd_simt(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
+template <typename R>
+int yzt_inv_simt(const dfno_geom&, const void*, double, void*, cudaStream_t);
+template <typename R>
+int xspec_fwd_simt(const dfno_geom&, const void*, const void*, void*, void*, cudaStream_t);
+template <typename R>
+int xspec_bwd_simt(const dfno_geom&, const void*, const void*, const void*, void*, void*, cudaStream_t);
+// tcgen05 tensor-core path (dft_yzt_tc.cu); returns DFNO_ERR_UNSUPPORTED
+// when the geometry is outside its envelope.
+int yzt_fwd_tc(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
+int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
+}  // namespace dfno
+
+using namespace dfno;
+
+namespace {
+
+int retained(int n, int m) { return (2 * m < n) ? 2 * m : n; }
+
+// Remainder-first block boundaries (reference d/partition.py:47-66).
+bool check_blocks(const int32_t* starts, int extent, int P) {
+  if (P < 1 || P > extent) return false;
+  const int base = extent / P, rem = extent % P;
+  int cur = 0;
+  for (int r = 0; r < P; ++r) {
+    if (starts[r] != cur) return false;
+    cur += base + (r < rem ? 1 : 0);
+  }
+  return starts[P] == extent;
+}
+
+// Environment switch for A/B measurements: DFNO_DISABLE_TC=1 forces SIMT.
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DFNO_DISABLE_TC");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+}  // namespace
+
+extern "C" int dfno_abi_version(void) { return DFNO_ABI_VERSION; }
+
+extern "C" const char* dfno_build_info(void) {
+#define DFNO_STR2(x) #x
+#define DFNO_STR(x) DFNO_STR2(x)
+  return "libdfno sm_100a (tcgen05 3xTF32 yzt DFT; SIMT fp32/fp64 generic path), nvcc " DFNO_STR(
+      __CUDACC_VER_MAJOR__) "." DFNO_STR(__CUDACC_VER_MINOR__);
+}
+
+extern "C" const char* dfno_status_string(int status) {
+  switch (status) {
+    case DFNO_OK: return "ok";
+    case DFNO_ERR_DIMENSION: return "dimension mismatch";
+    case DFNO_ERR_DTYPE: return "dtype mismatch (real32 / real64 only)";
+    case DFNO_ERR_INFEASIBLE: return "infeasible partition";
+    case DFNO_ERR_SHAPE: return "shape mismatch";
+    case DFNO_ERR_NULL: return "null pointer argument";
+    case DFNO_ERR_CUDA: return "CUDA launch failure";
+    case DFNO_ERR_UNSUPPORTED: return "geometry outside the kernel envelope";
+    default: return "unknown status";
+  }
+}
+
+// Feasibility rules of FnoConfig.__post_init__ (reference d/fno.py:77-96).
+extern "C" int dfno_geom_validate(const dfno_geom* g) {
+  if (!g) return DFNO_ERR_NULL;
+  if (g->dtype != DFNO_F32 && g->dtype != DFNO_F64) return DFNO_ERR_DTYPE;
+  if (g->batch < 0 || g->c_in < 1 || g->c < 1 || g->c_out < 1) return DFNO_ERR_DIMENSION;
+  if (g->nx < 1 || g->ny < 1 || g->nz < 1 || g->nt < 1) return DFNO_ERR_DIMENSION;
+  if (g->mx < 1 || g->my < 1 || g->mz < 1 || g->mt < 1) return DFNO_ERR_DIMENSION;
+  if (g->act < DFNO_ACT_RELU || g->act > DFNO_ACT_IDENTITY) return DFNO_ERR_DIMENSION;
+  if (g->rx != retained(g->nx, g->mx) || g->ry != retained(g->ny, g->my) || g->rz != retained(g->nz, g->mz) ||
+      g->rt != retained(g->nt, g->mt))
+    return DFNO_ERR_SHAPE;
+  if (g->nranks < 1 || g->nranks > DFNO_MAX_RANKS) return DFNO_ERR_INFEASIBLE;
+  if (g->nranks > g->nx || g->nranks > g->ry) return DFNO_ERR_INFEASIBLE;
+  if (g->rank < 0 || g->rank >= g->nranks) return DFNO_ERR_SHAPE;
+  if (!check_blocks(g->x_starts, g->nx, g->nranks)) return DFNO_ERR_SHAPE;
+  if (!check_blocks(g->ky_starts, g->ry, g->nranks)) return DFNO_ERR_SHAPE;
+  return DFNO_OK;
+}
+
+extern "C" int dfno_sizes(const dfno_geom* g, int64_t* xk_elems, int64_t* kx_elems, int64_t* spec_elems,
+                          int64_t* wshard_elems) {
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  const int64_t rzt = (int64_t)g->rz * g->rt;
+  const int64_t XL = x_local(*g), KYL = ky_local(*g);
+  if (xk_elems) *xk_elems = (int64_t)g->batch * g->c * XL * g->ry * rzt;
+  if (kx_elems) *kx_elems = (int64_t)g->batch * g->c * g->nx * KYL * rzt;
+  if (spec_elems) *spec_elems = (int64_t)g->batch * g->c * g->rx * KYL * rzt;
+  if (wshard_elems) *wshard_elems = (int64_t)g->c * g->c * g->rx * KYL * rzt;
+  return DFNO_OK;
+}
+
+extern "C" int dfno_dft_yzt_fwd(const dfno_geom* g, const void* src, const void* pre, int src_mode, double scale,
+                                void* xk_out, void* stream) {
+  if (!g || !src || !xk_out) return DFNO_ERR_NULL;
+  int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (src_mode == DFNO_SRC_GRAD && !pre) return DFNO_ERR_NULL;
+  if (src_mode < DFNO_SRC_ACT || src_mode > DFNO_SRC_RAW) return DFNO_ERR_DIMENSION;
+  if (g->batch == 0) return DFNO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32) {
+    if (tc_enabled()) {
+      rc = yzt_fwd_tc(*g, src, pre, src_mode, scale, xk_out, st);
+      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+    }
+    return yzt_fwd_simt<float>(*g, src, pre, src_mode, scale, xk_out, st);
+  }
+  return yzt_fwd_simt<double>(*g, src, pre, src_mode, scale, xk_out, st);
+}
+
+extern "C" int dfno_dft_yzt_inv(const dfno_geom* g, const void* xk_in, double scale, void* out, void* stream) {
+  if (!g || !xk_in || !out) return DFNO_ERR_NULL;
+  int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32) {
+    if (tc_enabled()) {
+      rc = yzt_inv_tc(*g, xk_in, scale, out, st);
+      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+    }
+    return yzt_inv_simt<float>(*g, xk_in, scale, out, st);
+  }
+  return yzt_inv_simt<double>(*g, xk_in, scale, out, st);
+}
+
+extern "C" int dfno_xspec_fwd(const dfno_geom* g, const void* kx_in, const void* w, void* spec, void* kx_out,
+                              void* stream) {
+  if (!g || !kx_in || !w || !kx_out) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32) return xspec_fwd_simt<float>(*g, kx_in, w, spec, kx_out, st);
+  return xspec_fwd_simt<double>(*g, kx_in, w, spec, kx_out, st);
+}
+
+extern "C" int dfno_xspec_bwd(const dfno_geom* g, const void* kx_in, const void* spec, const void* w, void* gw,
+                              void* kx_out, void* stream) {
+  if (!g || !kx_in || !spec || !w || !gw || !kx_out) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32) return xspec_bwd_simt<float>(*g, kx_in, spec, w, gw, kx_out, st);
+  return xspec_bwd_simt<double>(*g, kx_in, spec, w, gw, kx_out, st);
+}

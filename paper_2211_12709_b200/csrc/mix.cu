@@ -1,0 +1,426 @@
+// Point-wise channel mix (encoder / decoder) forward and backward.
+//
+// Forward replaces _mix_layer_forward (reference d/fno.py:286-289):
+// einsum_channel_mix (d/tensor.py:210-228) + activation (d/fno.py:41-46).
+// Backward replaces the mixer part of fno_backward (d/fno.py:484-486,
+// d/fno.py:497-499): g*act'(pre), _mix_weight_grad (d/fno.py:405-406) and
+// _mix_input_grad (d/fno.py:409-412).
+//
+// Both are HBM-streaming kernels: each thread owns VEC consecutive points of
+// one batch entry, reads every input channel once with vector loads, keeps the
+// (cin x CO) weight tile in shared memory (broadcast reads) and the CO output
+// accumulators in registers.  The weight gradient is a (cin x cout) reduction
+// over all points: per-CTA register-tiled 4x4 partial sums, reduced across
+// point groups with warp shuffles + shared memory, written as one partial per
+// CTA and summed in fixed order by k_reduce_partials (deterministic).
+#include "common.cuh"
+
+namespace dfno {
+
+template <typename R, int VEC>
+struct Vec;
+template <>
+struct Vec<float, 4> {
+  using T = float4;
+};
+template <>
+struct Vec<float, 2> {
+  using T = float2;
+};
+template <>
+struct Vec<double, 2> {
+  using T = double2;
+};
+template <typename R>
+struct Vec<R, 1> {
+  using T = R;
+};
+
+template <typename R, int VEC>
+__device__ __forceinline__ void ldv(const R* p, R (&v)[VEC]) {
+  if constexpr (VEC == 1) {
+    v[0] = __ldg(p);
+  } else {
+    typename Vec<R, VEC>::T t = __ldg(reinterpret_cast<const typename Vec<R, VEC>::T*>(p));
+    const R* tr = reinterpret_cast<const R*>(&t);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) v[k] = tr[k];
+  }
+}
+
+template <typename R, int VEC>
+__device__ __forceinline__ void stv(R* p, const R (&v)[VEC]) {
+  if constexpr (VEC == 1) {
+    p[0] = v[0];
+  } else {
+    typename Vec<R, VEC>::T t;
+    R* tr = reinterpret_cast<R*>(&t);
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) tr[k] = v[k];
+    *reinterpret_cast<typename Vec<R, VEC>::T*>(p) = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <typename R, int CO, int VEC>
+__global__ void __launch_bounds__(256) k_mix_fwd(long long npts, int nb, int cin, int cout, int o0,
+                                                 const R* __restrict__ src, int src_act, int act,
+                                                 const R* __restrict__ w, R* __restrict__ pre,
+                                                 R* __restrict__ post) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* ws = reinterpret_cast<R*>(smem_raw);  // [cin][CO]
+  for (int k = threadIdx.x; k < cin * CO; k += blockDim.x) {
+    const int i = k / CO, o = k % CO;
+    ws[k] = (o0 + o < cout) ? w[(long long)i * cout + o0 + o] : (R)0;
+  }
+  __syncthreads();
+  const long long nvec = npts / VEC;
+  const long long total = (long long)nb * nvec;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long bb = q / nvec;
+    const long long p = (q - bb * nvec) * VEC;
+    R acc[CO][VEC];
+#pragma unroll
+    for (int o = 0; o < CO; ++o)
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) acc[o][k] = (R)0;
+    const R* s = src + bb * cin * npts + p;
+    for (int i = 0; i < cin; ++i) {
+      R v[VEC];
+      ldv<R, VEC>(s + (long long)i * npts, v);
+      if (src_act) {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) v[k] = act_apply<R>(act, v[k]);
+      }
+      const R* wr = ws + i * CO;
+#pragma unroll
+      for (int o = 0; o < CO; ++o) {
+        const R wv = wr[o];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[o][k] = fma(v[k], wv, acc[o][k]);
+      }
+    }
+    R* pr = pre + bb * cout * npts + p;
+    R* po = post ? post + bb * cout * npts + p : nullptr;
+#pragma unroll
+    for (int o = 0; o < CO; ++o) {
+      if (o0 + o < cout) {
+        stv<R, VEC>(pr + (long long)(o0 + o) * npts, acc[o]);
+        if (po) {
+          R a[VEC];
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) a[k] = act_apply<R>(act, acc[o][k]);
+          stv<R, VEC>(po + (long long)(o0 + o) * npts, a);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+constexpr int kMixBwdThreads = 256;
+
+// CM = padded max(cin, cout) (multiple of 4).  One point per thread per tile.
+template <typename R, int CM>
+__global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
+    long long npts, int nb, int cin, int cout, const R* __restrict__ gout, const R* __restrict__ pre,
+    const R* __restrict__ src, int src_act, int act, const R* __restrict__ w, R* __restrict__ gin,
+    R* __restrict__ partials) {
+  constexpr int TP = kMixBwdThreads;
+  constexpr int NB4 = CM / 4;                 // 4-blocks per channel dim
+  constexpr int NPAIR = NB4 * NB4;            // (ib, ob) 4x4 tiles
+  constexpr int NGRP = (TP / NPAIR) > 0 ? (TP / NPAIR) : 1;  // point groups
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* ws = reinterpret_cast<R*>(smem_raw);     // [CM][CM] (i, o), zero padded
+  R* As = ws + CM * CM;                       // [TP][CM]  f(src) per point
+  R* Gs = As + TP * CM;                       // [TP][CM]  gp per point
+  R* red = Gs + TP * CM;                      // [NGRP][NPAIR*16] reduction
+
+  for (int k = threadIdx.x; k < CM * CM; k += blockDim.x) {
+    const int i = k / CM, o = k % CM;
+    ws[k] = (i < cin && o < cout) ? w[(long long)i * cout + o] : (R)0;
+  }
+
+  const int tid = threadIdx.x;
+  const int pair = tid % NPAIR;
+  const int grp = tid / NPAIR;
+  const bool reducer = (tid < NPAIR * NGRP);
+  const int ib = pair / NB4, ob = pair % NB4;
+  R acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = (R)0;
+
+  const long long total = (long long)nb * npts;
+  const long long ntiles = (total + TP - 1) / TP;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // previous tile's As/Gs fully consumed
+    const long long q = tile * TP + tid;
+    R gp[CM];
+    R av[CM];
+    if (q < total) {
+      const long long bb = q / npts, p = q - bb * npts;
+      const R* go = gout + bb * cout * npts + p;
+      const R* pr = pre + bb * cout * npts + p;
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        gp[o] = (R)0;
+        if (o < cout) gp[o] = __ldg(go + (long long)o * npts) * act_deriv<R>(act, __ldg(pr + (long long)o * npts));
+      }
+      const R* s = src + bb * cin * npts + p;
+#pragma unroll
+      for (int i = 0; i < CM; ++i) {
+        av[i] = (R)0;
+        if (i < cin) {
+          R v = __ldg(s + (long long)i * npts);
+          av[i] = src_act ? act_apply<R>(act, v) : v;
+        }
+      }
+      if (gin) {
+        R* gi = gin + bb * cin * npts + p;
+        for (int i = 0; i < cin; ++i) {
+          R sacc = (R)0;
+#pragma unroll
+          for (int o = 0; o < CM; ++o) sacc = fma(gp[o], ws[i * CM + o], sacc);
+          gi[(long long)i * npts] = sacc;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        gp[o] = (R)0;
+        av[o] = (R)0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CM; ++k) {
+      As[tid * CM + k] = av[k];
+      Gs[tid * CM + k] = gp[k];
+    }
+    __syncthreads();
+    if (reducer) {
+      for (int t = grp; t < TP; t += NGRP) {
+        const R* ar = As + t * CM + ib * 4;
+        const R* gr = Gs + t * CM + ob * 4;
+        R a4[4], g4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          a4[k] = ar[k];
+          g4[k] = gr[k];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(a4[a], g4[b], acc[a][b]);
+      }
+    }
+  }
+  // Cross-group reduction in fixed order.
+  __syncthreads();
+  if (reducer) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) red[grp * NPAIR * 16 + pair * 16 + a * 4 + b] = acc[a][b];
+  }
+  __syncthreads();
+  R* outp = partials + (long long)blockIdx.x * cin * cout;
+  for (int e = tid; e < NPAIR * 16; e += blockDim.x) {
+    R s = (R)0;
+    for (int gI = 0; gI < NGRP; ++gI) s += red[gI * NPAIR * 16 + e];
+    const int pr = e / 16, ab = e % 16;
+    const int i = (pr / NB4) * 4 + ab / 4;
+    const int o = (pr % NB4) * 4 + ab % 4;
+    if (i < cin && o < cout) outp[i * cout + o] = s;
+  }
+}
+
+template <typename R>
+__global__ void k_reduce_partials(int nparts, long long n, const R* __restrict__ partials, R* __restrict__ out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    R s = (R)0;
+    for (int k = 0; k < nparts; ++k) s += partials[(long long)k * n + e];
+    out[e] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename R, int CO, int VEC>
+static int launch_mix_fwd(long long npts, int nb, int cin, int cout, int o0, const void* src, int src_act,
+                          int act, const void* w, void* pre, void* post, cudaStream_t st) {
+  const size_t smem = (size_t)cin * CO * sizeof(R);
+  auto kern = k_mix_fwd<R, CO, VEC>;
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return DFNO_ERR_UNSUPPORTED;
+  }
+  const long long work = (long long)nb * (npts / VEC);
+  long long blocks = (work + 255) / 256;
+  const long long cap = (long long)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, 256, smem, st>>>(npts, nb, cin, cout, o0, (const R*)src, src_act, act, (const R*)w,
+                                            (R*)pre, (R*)post);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+template <typename R, int CO>
+static int mix_fwd_vec(long long npts, int nb, int cin, int cout, int o0, const void* src, int src_act, int act,
+                       const void* w, void* pre, void* post, cudaStream_t st) {
+  constexpr int V = sizeof(R) == 4 ? 4 : 2;
+  const bool aligned = (npts % V == 0) && ((uintptr_t)src % (V * sizeof(R)) == 0) &&
+                       ((uintptr_t)pre % (V * sizeof(R)) == 0) &&
+                       (post == nullptr || (uintptr_t)post % (V * sizeof(R)) == 0);
+  if (aligned) return launch_mix_fwd<R, CO, V>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+  return launch_mix_fwd<R, CO, 1>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+}
+
+template <typename R>
+static int mix_fwd_dispatch(long long npts, int nb, int cin, int cout, const void* src, int src_act, int act,
+                            const void* w, void* pre, void* post, cudaStream_t st) {
+  for (int o0 = 0; o0 < cout; o0 += 32) {
+    const int rem = cout - o0;
+    int rc;
+    if (rem <= 1) rc = mix_fwd_vec<R, 1>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 2) rc = mix_fwd_vec<R, 2>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 4) rc = mix_fwd_vec<R, 4>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 8) rc = mix_fwd_vec<R, 8>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 12) rc = mix_fwd_vec<R, 12>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 16) rc = mix_fwd_vec<R, 16>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 20) rc = mix_fwd_vec<R, 20>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else if (rem <= 24) rc = mix_fwd_vec<R, 24>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    else rc = mix_fwd_vec<R, 32>(npts, nb, cin, cout, o0, src, src_act, act, w, pre, post, st);
+    if (rc != DFNO_OK) return rc;
+  }
+  return DFNO_OK;
+}
+
+static int mix_bwd_cm(int cin, int cout) {
+  const int m = cin > cout ? cin : cout;
+  if (m <= 4) return 4;
+  if (m <= 8) return 8;
+  if (m <= 12) return 12;
+  if (m <= 16) return 16;
+  if (m <= 20) return 20;
+  if (m <= 24) return 24;
+  if (m <= 32) return 32;
+  return -1;
+}
+
+static int mix_bwd_blocks(long long npts, int nb) {
+  const long long tiles = ((long long)nb * npts + kMixBwdThreads - 1) / kMixBwdThreads;
+  long long blocks = (long long)num_sms() * 2;
+  if (blocks > tiles) blocks = tiles;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+template <typename R, int CM>
+static int launch_mix_bwd(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                          const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                          cudaStream_t st) {
+  constexpr int NB4 = CM / 4;
+  constexpr int NPAIR = NB4 * NB4;
+  constexpr int NGRP = (kMixBwdThreads / NPAIR) > 0 ? (kMixBwdThreads / NPAIR) : 1;
+  const size_t smem = sizeof(R) * ((size_t)CM * CM + 2 * (size_t)kMixBwdThreads * CM + (size_t)NGRP * NPAIR * 16);
+  auto kern = k_mix_bwd<R, CM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  const int blocks = mix_bwd_blocks(npts, nb);
+  kern<<<blocks, kMixBwdThreads, smem, st>>>(npts, nb, cin, cout, (const R*)gout, (const R*)pre, (const R*)src,
+                                             src_act, act, (const R*)w, (R*)gin, (R*)partials);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+template <typename R>
+static int mix_bwd_dispatch(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                            const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                            cudaStream_t st) {
+  switch (mix_bwd_cm(cin, cout)) {
+    case 4: return launch_mix_bwd<R, 4>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 8: return launch_mix_bwd<R, 8>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 12: return launch_mix_bwd<R, 12>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 16: return launch_mix_bwd<R, 16>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 20: return launch_mix_bwd<R, 20>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 24: return launch_mix_bwd<R, 24>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    case 32: return launch_mix_bwd<R, 32>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+    default: return DFNO_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace dfno
+
+using namespace dfno;
+
+extern "C" int dfno_mix_fwd(const dfno_geom* g, int64_t npts, int cin, int cout, const void* src, int src_act,
+                            const void* w, void* pre, void* post, void* stream) {
+  if (!g || !src || !w || !pre) return DFNO_ERR_NULL;
+  if (npts < 0 || cin < 1 || cout < 1) return DFNO_ERR_DIMENSION;
+  if (npts == 0 || g->batch == 0) return DFNO_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32)
+    return mix_fwd_dispatch<float>(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
+  if (g->dtype == DFNO_F64)
+    return mix_fwd_dispatch<double>(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
+  return DFNO_ERR_DTYPE;
+}
+
+extern "C" int dfno_mix_bwd_partials(const dfno_geom* g, int64_t npts, int cin, int cout, int64_t* partial_elems,
+                                     int* num_partials) {
+  if (!g || !partial_elems || !num_partials) return DFNO_ERR_NULL;
+  if (mix_bwd_cm(cin, cout) < 0) return DFNO_ERR_UNSUPPORTED;
+  const int blocks = mix_bwd_blocks(npts, g->batch);
+  *num_partials = blocks;
+  *partial_elems = (int64_t)blocks * cin * cout;
+  return DFNO_OK;
+}
+
+extern "C" int dfno_mix_bwd(const dfno_geom* g, int64_t npts, int cin, int cout, const void* gout, const void* pre,
+                            const void* src, int src_act, const void* w, void* gin, void* partials, void* stream) {
+  if (!g || !gout || !pre || !src || !w || !partials) return DFNO_ERR_NULL;
+  if (npts < 1 || cin < 1 || cout < 1) return DFNO_ERR_DIMENSION;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g->dtype == DFNO_F32)
+    return mix_bwd_dispatch<float>(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials, st);
+  if (g->dtype == DFNO_F64)
+    return mix_bwd_dispatch<double>(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
+                                    st);
+  return DFNO_ERR_DTYPE;
+}
+
+extern "C" int dfno_reduce_partials(const dfno_geom* g, int num_partials, int64_t n, const void* partials, void* out,
+                                    void* stream) {
+  if (!g || !partials || !out) return DFNO_ERR_NULL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = (int)((n + 255) / 256);
+  if (g->dtype == DFNO_F32)
+    k_reduce_partials<float><<<blocks, 256, 0, st>>>(num_partials, n, (const float*)partials, (float*)out);
+  else if (g->dtype == DFNO_F64)
+    k_reduce_partials<double><<<blocks, 256, 0, st>>>(num_partials, n, (const double*)partials, (double*)out);
+  else
+    return DFNO_ERR_DTYPE;
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
