@@ -392,35 +392,39 @@ class _Plan:
         return self.partials[key]
 
     # -- kernels -----------------------------------------------------------
-    def mix_fwd(self, cin, cout, src, src_act, w, pre, post):
-        _lib.check(self.lib.dfno_mix_fwd(self.gp, self.npts, cin, cout, _lib.ptr(src), int(src_act), _lib.ptr(w),
-                                         _lib.ptr(pre), _lib.ptr(post), _lib.stream_handle()), "dfno_mix_fwd")
+    def mix_fwd(self, cin, cout, src, src_act, w, pre, post, tag="mix_fwd"):
+        _launch(tag, lambda: _lib.check(self.lib.dfno_mix_fwd(
+            self.gp, self.npts, cin, cout, _lib.ptr(src), int(src_act), _lib.ptr(w), _lib.ptr(pre), _lib.ptr(post),
+            _lib.stream_handle()), "dfno_mix_fwd"))
 
-    def mix_bwd(self, cin, cout, gout, pre, src, src_act, w, gin) -> torch.Tensor:
+    def mix_bwd(self, cin, cout, gout, pre, src, src_act, w, gin, tag="mix_bwd") -> torch.Tensor:
         buf, nparts = self.partial_buf(cin, cout)
-        _lib.check(self.lib.dfno_mix_bwd(self.gp, self.npts, cin, cout, _lib.ptr(gout), _lib.ptr(pre), _lib.ptr(src),
-                                         int(src_act), _lib.ptr(w), _lib.ptr(gin), _lib.ptr(buf),
-                                         _lib.stream_handle()), "dfno_mix_bwd")
+        _launch(f"mix_bwd.{tag}", lambda: _lib.check(self.lib.dfno_mix_bwd(
+            self.gp, self.npts, cin, cout, _lib.ptr(gout), _lib.ptr(pre), _lib.ptr(src), int(src_act), _lib.ptr(w),
+            _lib.ptr(gin), _lib.ptr(buf), _lib.stream_handle()), "dfno_mix_bwd"))
         gw = torch.empty((cin, cout), dtype=self.real, device=self.device)
-        _lib.check(self.lib.dfno_reduce_partials(self.gp, nparts, cin * cout, _lib.ptr(buf), _lib.ptr(gw),
-                                                 _lib.stream_handle()), "dfno_reduce_partials")
+        _launch(f"reduce.{tag}", lambda: _lib.check(self.lib.dfno_reduce_partials(
+            self.gp, nparts, cin * cout, _lib.ptr(buf), _lib.ptr(gw), _lib.stream_handle()), "dfno_reduce_partials"))
         return gw
 
-    def yzt_fwd(self, src, pre, mode, scale, out):
-        _lib.check(self.lib.dfno_dft_yzt_fwd(self.gp, _lib.ptr(src), _lib.ptr(pre), mode, float(scale), _lib.ptr(out),
-                                             _lib.stream_handle()), "dfno_dft_yzt_fwd")
+    def yzt_fwd(self, src, pre, mode, scale, out, tag="yzt_fwd"):
+        _launch(tag, lambda: _lib.check(self.lib.dfno_dft_yzt_fwd(
+            self.gp, _lib.ptr(src), _lib.ptr(pre), mode, float(scale), _lib.ptr(out), _lib.stream_handle()),
+            "dfno_dft_yzt_fwd"))
 
-    def yzt_inv(self, xk_in, scale, out):
-        _lib.check(self.lib.dfno_dft_yzt_inv(self.gp, _lib.ptr(xk_in), float(scale), _lib.ptr(out),
-                                             _lib.stream_handle()), "dfno_dft_yzt_inv")
+    def yzt_inv(self, xk_in, scale, out, tag="yzt_inv"):
+        _launch(tag, lambda: _lib.check(self.lib.dfno_dft_yzt_inv(
+            self.gp, _lib.ptr(xk_in), float(scale), _lib.ptr(out), _lib.stream_handle()), "dfno_dft_yzt_inv"))
 
     def xspec_fwd(self, kx_in, w, spec, kx_out):
-        _lib.check(self.lib.dfno_xspec_fwd(self.gp, _lib.ptr(kx_in), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(kx_out),
-                                           _lib.stream_handle()), "dfno_xspec_fwd")
+        _launch("xspec_fwd", lambda: _lib.check(self.lib.dfno_xspec_fwd(
+            self.gp, _lib.ptr(kx_in), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(kx_out), _lib.stream_handle()),
+            "dfno_xspec_fwd"))
 
     def xspec_bwd(self, kx_in, spec, w, gw, kx_out):
-        _lib.check(self.lib.dfno_xspec_bwd(self.gp, _lib.ptr(kx_in), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw),
-                                           _lib.ptr(kx_out), _lib.stream_handle()), "dfno_xspec_bwd")
+        _launch("xspec_bwd", lambda: _lib.check(self.lib.dfno_xspec_bwd(
+            self.gp, _lib.ptr(kx_in), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw), _lib.ptr(kx_out),
+            _lib.stream_handle()), "dfno_xspec_bwd"))
 
     # -- exchanges (reference fno.py:330, :337, :449, :458) ---------------
     def x_to_ky(self, comm: Communicator, label: str) -> torch.Tensor:
@@ -440,6 +444,21 @@ class _Plan:
 
 _PLANS: dict = {}
 _PLANS_LOCK = threading.Lock()
+_TIMER = None
+
+
+def set_kernel_timer(timer) -> None:
+    """Install ``timer(name, launch_fn)`` around every libdfno launch (used by
+    bench.py to time kernels with CUDA events); None removes it."""
+    global _TIMER
+    _TIMER = timer
+
+
+def _launch(name: str, fn) -> None:
+    if _TIMER is None:
+        fn()
+    else:
+        _TIMER(name, fn)
 
 
 def _plan(config: FnoConfig, comm: Communicator, batch: int) -> _Plan:
@@ -501,7 +520,7 @@ def _mix_forward(comm, plan: _Plan, src: torch.Tensor, src_act: bool, w: DenseTe
         raise DimensionMismatchError(f"{label} weight shape {tuple(wt.shape)}, expected {(cin, cout)}")
     pre = plan.empty_act(cout)
     post = plan.empty_act(cout) if want_post else None
-    plan.mix_fwd(cin, cout, src, src_act, wt, pre, post)
+    plan.mix_fwd(cin, cout, src, src_act, wt, pre, post, tag="mix_fwd.enc" if label == "encoder" else "mix_fwd.dec")
     return pre, post, w_used
 
 
@@ -550,13 +569,13 @@ def _block_forward(comm, plan: _Plan, src: torch.Tensor, mode: int, w: torch.Ten
                    want_spec: bool):
     """fft_yzt -> truncate -> R(x->ky) -> fft_x -> truncate -> W -> pad ->
     ifft_x -> R(ky->x) -> pad -> ifft_yzt -> real  (reference fno.py:309-347)."""
-    plan.yzt_fwd(src, None, mode, 1.0, plan.buf_a)
+    plan.yzt_fwd(src, None, mode, 1.0, plan.buf_a, tag="yzt_fwd.fwd")
     kx_in = plan.x_to_ky(comm, f"{label}.fwd.x->ky")
     spec = torch.empty(plan.spec_shape, dtype=plan.cplx, device=plan.device) if want_spec else None
     plan.xspec_fwd(kx_in, w, spec, plan.buf_c)
     xk_in = plan.ky_to_x(comm, plan.buf_c, f"{label}.fwd.ky->x")
     pre = plan.empty_act(plan.config.hidden_channels)
-    plan.yzt_inv(xk_in, 1.0 / plan.n_yzt, pre)
+    plan.yzt_inv(xk_in, 1.0 / plan.n_yzt, pre, tag="yzt_inv.fwd")
     return pre, spec
 
 
@@ -619,13 +638,13 @@ def _block_backward(comm, plan: _Plan, g: torch.Tensor, pre: Optional[torch.Tens
     """Adjoint chain (reference fno.py:445-464): fft_yzt/N_yzt -> truncate ->
     R(x->ky) -> fft_x/Nx -> truncate -> gW, dX -> pad -> ifft_x*Nx -> R(ky->x)
     -> pad -> ifft_yzt*N_yzt -> real."""
-    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a)
+    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a, tag="yzt_fwd.bwd")
     kx_in = plan.x_to_ky(comm, f"{label}.bwd.x->ky")
     gw = torch.empty(plan.w_shape, dtype=plan.cplx, device=plan.device)
     plan.xspec_bwd(kx_in, spec, w, gw, plan.buf_c)
     xk_in = plan.ky_to_x(comm, plan.buf_c, f"{label}.bwd.ky->x")
     gin = plan.empty_act(plan.config.hidden_channels)
-    plan.yzt_inv(xk_in, 1.0, gin)
+    plan.yzt_inv(xk_in, 1.0, gin, tag="yzt_inv.bwd")
     return gin, gw
 
 
@@ -657,7 +676,7 @@ def fno_backward(comm: Communicator, g_local: DenseTensor, params: FnoParams, co
     dec_w = _on_device(cache.dec_w, plan, plan.real, "decoder weight")
     last_pre = cache.blocks[-1].pre_activation.data
     g_a = plan.empty_act(c)
-    gwd_local = plan.mix_bwd(c, config.out_channels, g, cache.dec_pre.data, last_pre, True, dec_w, g_a)
+    gwd_local = plan.mix_bwd(c, config.out_channels, g, cache.dec_pre.data, last_pre, True, dec_w, g_a, tag="dec")
 
     block_grads = [None] * L
     for i in reversed(range(L)):
@@ -669,7 +688,8 @@ def fno_backward(comm: Communicator, g_local: DenseTensor, params: FnoParams, co
 
     enc_w = _on_device(cache.enc_w, plan, plan.real, "encoder weight")
     gx = plan.empty_act(config.in_channels)
-    gwe_local = plan.mix_bwd(config.in_channels, c, g_a, cache.enc_pre.data, cache.x_in.data, False, enc_w, gx)
+    gwe_local = plan.mix_bwd(config.in_channels, c, g_a, cache.enc_pre.data, cache.x_in.data, False, enc_w, gx,
+                             tag="enc")
 
     labels = (DimLabel.C, DimLabel.CO)
     gwe = comm.reduce_sum(DenseTensor(labels, gwe_local), root=0, label="bwd.we")
