@@ -1,11 +1,782 @@
-// tcgen05 (5th-generation tensor core) path for the truncated yzt DFT.
-// Placeholder until the 3xTF32 kernels land: reports the geometry as outside
-// its envelope so dispatch uses the SIMT kernels.
+// Truncated (y, z, t) DFTs on the 5th-generation tensor cores (tcgen05,
+// kind::tf32, fp32 accumulation in TMEM) with 3xTF32 operand splitting
+// (hi*hi + lo*hi + hi*lo, round-to-nearest split), so results carry
+// fp32-level accuracy; tests/test_gpu_kernels.py checks them against numpy
+// real64.
+//
+// FORWARD (replaces fft_dims(a,(y,z,t)) + truncate_modes, reference
+// d/fno.py:328-329; backward use d/fno.py:446-448).  A persistent CTA walks
+// (b, c, x) slabs; each slab is consumed in tiles of 8 y-planes x 16 z-rows x
+// 32 t, streamed into a ring of raw shared-memory stages with cp.async
+// (several tiles in flight per SM), then converted (activation or
+// grad*act' fused, 3xTF32 split) into the stage-T operand:
+//
+//   stage T  D1[(y,z)][kt re|im] = sum_t f(a)[y][z][t] {cos,-sin}      M=128 N=32 K=32
+//   stage Z  D2[(kt,y)][kz]     += sum_z D1 e^{-i kz z} (planar re/im)  M=128 N=16 K=16 per tile
+//   stage Y  D3[(kz,kt)][ky]    += sum_y D2 e^{-i ky y}  (per 8 y)      M=2x128 N=16 K=8
+//
+// INVERSE (replaces pad_modes + ifft_dims(yzt) + .real, d/fno.py:338-343 /
+// d/fno.py:459-464), per slab, per 16-y chunk:
+//
+//   stage Y' D1[(kz,kt)][y]  = sum_ky V e^{+i ky y}                    M=2x128 N=16 K=16
+//   stage Z' D2[(y,kt)][z]   = sum_kz D1 e^{+i kz z}                   M=2x128 N<=64 K=16
+//   stage T' D3[(y,z)][t]    = Re sum_kt D2 e^{+i kt t}  (real output)  M=2x128 N=32 K=16
+//
+// The transposes between stages go TMEM -> registers -> shared memory into
+// SWIZZLE_NONE K-major tiles whose LBO / SBO paddings make the stores
+// bank-conflict free.  Twiddles are generated per CTA with exact integer
+// phase reduction (double precision) and split hi / lo.  The forward writes
+// straight into the peer-major XK exchange layout; the inverse reads it.
+//
+// Envelope: r_y, r_z, r_t <= 16 (m <= 8 per dim -- every BASELINE config);
+// other geometries use the SIMT kernels (dft_yzt.cu).
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace dfno {
-int yzt_fwd_tc(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t) {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTileT = 32;                         // t per stage-T K block
+constexpr int kRawBytes = 128 * kTileT * 4;        // one raw staged tile (16 KB)
+// forward operand tiles (bytes)
+constexpr int kLboT = 144, kSboT = 1152, kATBytes = 16 * kSboT;
+constexpr int kLboZ = 160, kSboZ = 608, kAZBytes = 16 * kSboZ;
+constexpr int kLboY = 192, kSboY = 320, kTileYBytes = 16 * kSboY;
+constexpr int kAYBytes = 8 * kTileYBytes;          // (re, im) x (hi, lo) x 2 tiles
+constexpr int kATRegion = (2 * kATBytes > kAYBytes) ? 2 * kATBytes : kAYBytes;  // A_T aliases A_Y
+// inverse operand tiles: 128 rows x K = 16, LBO 128, SBO 528
+constexpr int kSbo16 = 528, kTile16 = 16 * kSbo16;
+constexpr int kBSbo16 = 512;                       // twiddle B with K = 16
+constexpr uint32_t kFwdTmemCols = 128, kInvTmemCols = 512;
+
+__host__ __device__ inline int rup(int a, int b) { return (a + b - 1) / b * b; }
+
+__device__ __forceinline__ int kmaj(int r, int k, int lbo, int sbo) {
+  return (r >> 3) * sbo + (k >> 2) * lbo + (r & 7) * 16 + (k & 3) * 4;
+}
+
+__device__ __forceinline__ void st_split(unsigned char* hi, unsigned char* lo, int off, float v) {
+  float h, l;
+  tc::split_rn(v, h, l);
+  *reinterpret_cast<float*>(hi + off) = h;
+  *reinterpret_cast<float*>(lo + off) = l;
+}
+
+// hi / lo of a double-precision twiddle
+__device__ __forceinline__ void split_d(double v, float& hi, float& lo) {
+  hi = tc::round_tf32((float)v);
+  lo = tc::round_tf32((float)(v - (double)hi));
+}
+
+__device__ __forceinline__ void sincos_idx(long long k, int n, int N, double& s, double& c) {
+  const long long idx = (k * n) % N;
+  sincospi(2.0 * (double)idx / N, &s, &c);
+}
+
+template <int MODE>
+__device__ __forceinline__ float transform(float v, float p, int act) {
+  if (MODE == DFNO_SRC_ACT) return act == DFNO_ACT_GELU ? tc::gelu_fast(v) : act_apply<float>(act, v);
+  if (MODE == DFNO_SRC_GRAD) return v * (act == DFNO_ACT_GELU ? tc::gelu_grad_fast(p) : act_deriv<float>(act, p));
+  return v;
+}
+
+// Twiddle matrix B[n][k] (rows n, K-major, LBO 128) with 4 planes
+// (C hi, C lo, S hi, S lo): C = cos(2 pi f(n or k) ...), filled by fn(n, k, c, s).
+template <typename F>
+__device__ void fill_cs(unsigned char* b, int rows, int kdim, int sbo, F fn) {
+  const int plane = (rows / 8) * sbo;
+  for (int e = threadIdx.x; e < rows * kdim; e += blockDim.x) {
+    const int n = e / kdim, k = e % kdim;
+    double c = 0.0, s = 0.0;
+    fn(n, k, c, s);
+    float ch, cl, sh, sl;
+    split_d(c, ch, cl);
+    split_d(s, sh, sl);
+    const int off = kmaj(n, k, 128, sbo);
+    *reinterpret_cast<float*>(b + 0 * plane + off) = ch;
+    *reinterpret_cast<float*>(b + 1 * plane + off) = cl;
+    *reinterpret_cast<float*>(b + 2 * plane + off) = sh;
+    *reinterpret_cast<float*>(b + 3 * plane + off) = sl;
+  }
+}
+
+// 3xTF32 complex-planar MMA group:  D += A * B  for one K step where
+// A = a_{hi,lo}, B = b_{hi,lo}:  hi*hi + lo*hi + hi*lo.
+__device__ __forceinline__ void mma3(uint32_t d, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                     uint32_t idesc, uint32_t acc) {
+  tc::mma_tf32(d, a_hi, b_hi, idesc, acc);
+  tc::mma_tf32(d, a_lo, b_hi, idesc, 1u);
+  tc::mma_tf32(d, a_hi, b_lo, idesc, 1u);
+}
+
+struct FwdLayout {
+  int KT, NZ16, NY8, sbo_bt, sbo_bz, sbo_by, stages, stage_bytes;
+  int off_raw, off_at, off_az, off_bt, off_bz, off_by, total;
+};
+
+__host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt, int stages, bool grad) {
+  FwdLayout L;
+  L.KT = rup(nt, kTileT);
+  L.NZ16 = rup(nz, 16);
+  L.NY8 = rup(ny, 8);
+  L.sbo_bt = (L.KT / 4) * 128;
+  L.sbo_bz = (L.NZ16 / 4) * 128;
+  L.sbo_by = (L.NY8 / 4) * 128;
+  L.stages = stages;
+  L.stage_bytes = kRawBytes * (grad ? 2 : 1);
+  int o = 0;
+  L.off_raw = o; o += stages * L.stage_bytes;
+  L.off_at = o;  o += kATRegion;
+  L.off_az = o;  o += 4 * kAZBytes;
+  L.off_bt = o;  o += 2 * 4 * L.sbo_bt;
+  L.off_bz = o;  o += 4 * 2 * L.sbo_bz;
+  L.off_by = o;  o += 4 * 2 * L.sbo_by;
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+// ===========================================================================
+// forward
+// ===========================================================================
+template <int MODE, bool VEC, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, const float* __restrict__ src,
+                                                            const float* __restrict__ pre, float scale,
+                                                            float2* __restrict__ out) {
+  constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
+  constexpr int D = STAGES - 1;  // prefetch distance (tiles in flight)
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar_t, bar_z, bar_y;
+  __shared__ uint32_t tmem_base;
+
+  const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
+  const int XL = x_local(g);
+  const FwdLayout L = fwd_layout(Ny, Nz, Nt, STAGES, GRAD);
+  unsigned char* raw = smem + L.off_raw;
+  unsigned char* at_hi = smem + L.off_at;
+  unsigned char* at_lo = at_hi + kATBytes;
+  unsigned char* ay = smem + L.off_at;  // aliases A_T (used after the last stage-T of a chunk)
+  unsigned char* az = smem + L.off_az;
+  unsigned char* bt = smem + L.off_bt;
+  unsigned char* bz = smem + L.off_bz;
+  unsigned char* by = smem + L.off_by;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- twiddles ---------------------------------------------------------
+  {
+    const int plane = 4 * L.sbo_bt;  // 32 rows
+    for (int e = tid; e < 32 * L.KT; e += kThreads) {
+      const int n = e / L.KT, t = e % L.KT, kt = n & 15;
+      double c = 0.0, s = 0.0;
+      if (kt < g.rt && t < Nt) sincos_idx(mode_freq(kt, Nt, g.mt), t, Nt, s, c);
+      float hi, lo;
+      split_d(n < 16 ? c : -s, hi, lo);
+      const int off = kmaj(n, t, 128, L.sbo_bt);
+      *reinterpret_cast<float*>(bt + off) = hi;
+      *reinterpret_cast<float*>(bt + plane + off) = lo;
+    }
+  }
+  fill_cs(bz, 16, L.NZ16, L.sbo_bz, [&](int n, int z, double& c, double& s) {
+    if (n < g.rz && z < Nz) sincos_idx(mode_freq(n, Nz, g.mz), z, Nz, s, c);
+  });
+  fill_cs(by, 16, L.NY8, L.sbo_by, [&](int n, int y, double& c, double& s) {
+    if (n < g.ry && y < Ny) sincos_idx(mode_freq(n, Ny, g.my), y, Ny, s, c);
+  });
+  if (warp == 0) tc::tmem_alloc<kFwdTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar_t, 1);
+    tc::mbar_init(&bar_z, 1);
+    tc::mbar_init(&bar_y, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t d1 = tmem, d2 = tmem + 32, d3 = tmem + 64;
+
+  const int n_yc = (Ny + 7) / 8, n_zb = (Nz + 15) / 16, n_tb = L.KT / kTileT;
+  const int tiles_per_slab = n_yc * n_zb * n_tb;
+  const int slabs = g.batch * g.c * XL;
+  const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int total = my_slabs * tiles_per_slab;
+  const long long plane = (long long)Nz * Nt;
+  const int quarter = warp & 3, part = warp >> 2;
+
+  const uint32_t id_t = tc::idesc_tf32(128, 32);
+  const uint32_t id16 = tc::idesc_tf32(128, 16);
+  const uint32_t id16n = tc::idesc_tf32(128, 16, false, true);
+  const uint32_t s_at_hi = tc::smem_u32(at_hi), s_at_lo = tc::smem_u32(at_lo);
+  const uint32_t s_az = tc::smem_u32(az), s_ay = tc::smem_u32(ay);
+  const uint32_t s_bt = tc::smem_u32(bt), s_bz = tc::smem_u32(bz), s_by = tc::smem_u32(by);
+
+  // tile i -> (slab, yc, zb, tb)
+  auto coords = [&](int i, int& slab, int& yc, int& zb, int& tb) {
+    const int sl = i / tiles_per_slab, r = i % tiles_per_slab;
+    slab = (int)blockIdx.x + sl * (int)gridDim.x;
+    yc = r / (n_zb * n_tb);
+    zb = (r / n_tb) % n_zb;
+    tb = r % n_tb;
+  };
+  auto slab_base = [&](int slab) -> long long {
+    const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+    return (((long long)bb * g.c + ch) * XL + xl) * (long long)Ny * plane;
+  };
+  // issue the cp.async copies of tile i into its ring stage
+  auto issue = [&](int i) {
+    if (i < total) {
+      int slab, yc, zb, tb;
+      coords(i, slab, yc, zb, tb);
+      const long long sb = slab_base(slab);
+      unsigned char* st = raw + (i % STAGES) * L.stage_bytes;
+      const int y0 = yc * 8, z0 = zb * 16, t0 = tb * kTileT;
+      if (VEC) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = tid + kThreads * j, row = q >> 3, c4 = q & 7;
+          const int y = y0 + (row >> 4), z = z0 + (row & 15), t = t0 + 4 * c4;
+          const bool ok = (y < Ny) && (z < Nz) && (t < Nt);
+          const long long go = ok ? sb + (long long)y * plane + (long long)z * Nt + t : sb;
+          tc::cp16(st + row * 128 + c4 * 16, src + go, ok);
+          if (GRAD) tc::cp16(st + kRawBytes + row * 128 + c4 * 16, pre + go, ok);
+        }
+      } else {
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+          const int e = tid + kThreads * j, row = e >> 5, tt = e & 31;
+          const int y = y0 + (row >> 4), z = z0 + (row & 15), t = t0 + tt;
+          const bool ok = (y < Ny) && (z < Nz) && (t < Nt);
+          const long long go = ok ? sb + (long long)y * plane + (long long)z * Nt + t : sb;
+          tc::cp4(st + row * 128 + tt * 4, src + go, ok);
+          if (GRAD) tc::cp4(st + kRawBytes + row * 128 + tt * 4, pre + go, ok);
+        }
+      }
+    }
+    tc::cp_commit();
+  };
+
+  uint32_t ph_t = 0, ph_z = 0, ph_y = 0;
+  bool t_pending = false, z_pending = false, y_pending = false;
+#pragma unroll 1
+  for (int p = 0; p < D; ++p) issue(p);
+
+#pragma unroll 1
+  for (int i = 0; i < total; ++i) {
+    int slab, yc, zb, tb;
+    coords(i, slab, yc, zb, tb);
+    issue(i + D);
+    tc::cp_wait<D>();
+    // A_T / A_Y must be free: stage-T of the previous tile and stage-Y of the previous chunk done
+    if (t_pending) {
+      tc::mbar_wait(&bar_t, ph_t);
+      ph_t ^= 1;
+      t_pending = false;
+    }
+    if (y_pending) {
+      tc::mbar_wait(&bar_y, ph_y);
+      ph_y ^= 1;
+      y_pending = false;
+    }
+    // ---- convert the staged raw tile into the stage-T operand (hi / lo)
+    {
+      const unsigned char* st = raw + (i % STAGES) * L.stage_bytes;
+      if (VEC) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = tid + kThreads * j, row = q >> 3, c4 = q & 7;
+          float4 v = *reinterpret_cast<const float4*>(st + row * 128 + c4 * 16);
+          float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (GRAD) p = *reinterpret_cast<const float4*>(st + kRawBytes + row * 128 + c4 * 16);
+          v.x = transform<MODE>(v.x, p.x, g.act);
+          v.y = transform<MODE>(v.y, p.y, g.act);
+          v.z = transform<MODE>(v.z, p.z, g.act);
+          v.w = transform<MODE>(v.w, p.w, g.act);
+          float4 h, l;
+          tc::split_rn(v.x, h.x, l.x);
+          tc::split_rn(v.y, h.y, l.y);
+          tc::split_rn(v.z, h.z, l.z);
+          tc::split_rn(v.w, h.w, l.w);
+          const int off = (row >> 3) * kSboT + c4 * kLboT + (row & 7) * 16;
+          *reinterpret_cast<float4*>(at_hi + off) = h;
+          *reinterpret_cast<float4*>(at_lo + off) = l;
+        }
+      } else {
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+          const int e = tid + kThreads * j, row = e >> 5, tt = e & 31;
+          float v = *reinterpret_cast<const float*>(st + row * 128 + tt * 4);
+          const float p = GRAD ? *reinterpret_cast<const float*>(st + kRawBytes + row * 128 + tt * 4) : 0.f;
+          st_split(at_hi, at_lo, kmaj(row, tt, kLboT, kSboT), transform<MODE>(v, p, g.act));
+        }
+      }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    // ---- stage T
+    if (tid == 0) {
+      tc::fence_after();
+#pragma unroll
+      for (int s = 0; s < kTileT / 8; ++s) {
+        const uint32_t ka = 2 * s * kLboT, kb = (uint32_t)(tb * (kTileT / 4) + 2 * s) * 128;
+        mma3(d1, tc::desc(s_at_hi + ka, kLboT, kSboT), tc::desc(s_at_lo + ka, kLboT, kSboT),
+             tc::desc(s_bt + kb, 128, L.sbo_bt), tc::desc(s_bt + 4 * L.sbo_bt + kb, 128, L.sbo_bt), id_t,
+             (tb > 0 || s > 0) ? 1u : 0u);
+      }
+      tc::commit(&bar_t);
+    }
+    t_pending = true;
+    if (tb != n_tb - 1) continue;
+
+    // ---- epilogue T -> A_Z (needs D1; A_Z released by the previous stage Z)
+    tc::mbar_wait(&bar_t, ph_t);
+    ph_t ^= 1;
+    t_pending = false;
+    if (z_pending) {
+      tc::mbar_wait(&bar_z, ph_z);
+      ph_z ^= 1;
+      z_pending = false;
+    }
+    tc::fence_after();
+    {
+      float v[16];
+      tc::tmem_ld16(d1 + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
+      const int r = 32 * quarter + lane, y = r >> 4, zl = r & 15;  // D1 row = (y, zl)
+      unsigned char* hi = az + part * 2 * kAZBytes;
+      unsigned char* lo = hi + kAZBytes;
+      const int base = (zl >> 2) * kLboZ + y * 16 + (zl & 3) * 4;  // A_Z row = (kt, y), k = zl
+#pragma unroll
+      for (int kt = 0; kt < 16; ++kt) st_split(hi, lo, kt * kSboZ + base, v[kt]);
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    // ---- stage Z (K block zb = 16 z = 2 K steps), planar complex
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t pl = 2 * L.sbo_bz;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const uint32_t ka = 2 * s * kLboZ, kb = (uint32_t)(zb * 4 + 2 * s) * 128;
+        const uint64_t re_h = tc::desc(s_az + 0 * kAZBytes + ka, kLboZ, kSboZ);
+        const uint64_t re_l = tc::desc(s_az + 1 * kAZBytes + ka, kLboZ, kSboZ);
+        const uint64_t im_h = tc::desc(s_az + 2 * kAZBytes + ka, kLboZ, kSboZ);
+        const uint64_t im_l = tc::desc(s_az + 3 * kAZBytes + ka, kLboZ, kSboZ);
+        const uint64_t c_h = tc::desc(s_bz + 0 * pl + kb, 128, L.sbo_bz);
+        const uint64_t c_l = tc::desc(s_bz + 1 * pl + kb, 128, L.sbo_bz);
+        const uint64_t s_h = tc::desc(s_bz + 2 * pl + kb, 128, L.sbo_bz);
+        const uint64_t s_l = tc::desc(s_bz + 3 * pl + kb, 128, L.sbo_bz);
+        const uint32_t first = (zb == 0 && s == 0) ? 0u : 1u;
+        // e^{-i}: re += A_re C + A_im S ;  im += A_im C - A_re S
+        mma3(d2, re_h, re_l, c_h, c_l, id16, first);
+        mma3(d2, im_h, im_l, s_h, s_l, id16, 1u);
+        mma3(d2 + 16, im_h, im_l, c_h, c_l, id16, first);
+        mma3(d2 + 16, re_h, re_l, s_h, s_l, id16n, 1u);
+      }
+      tc::commit(&bar_z);
+    }
+    z_pending = true;
+    if (zb != n_zb - 1) continue;
+
+    // ---- epilogue Z -> A_Y (A_Y aliases A_T: stage T of this tile is done)
+    tc::mbar_wait(&bar_z, ph_z);
+    ph_z ^= 1;
+    z_pending = false;
+    tc::fence_after();
+    {
+      float v[16];
+      tc::tmem_ld16(d2 + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
+      const int m = 32 * quarter + lane, kt = m >> 3, y = m & 7;  // D2 row = (kt, y)
+      unsigned char* hi = ay + part * 4 * kTileYBytes;
+      unsigned char* lo = hi + 2 * kTileYBytes;
+      const int base = (kt >> 3) * kSboY + (y >> 2) * kLboY + (kt & 7) * 16 + (y & 3) * 4;
+#pragma unroll
+      for (int kz = 0; kz < 16; ++kz)  // A_Y row = (kz % 8, kt) in tile kz / 8, k = y
+        st_split(hi, lo, (kz >> 3) * kTileYBytes + (kz & 7) * 2 * kSboY + base, v[kz]);
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    // ---- stage Y (K = the 8 y of chunk yc)
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t kb = (uint32_t)(yc * 2) * 128, pl = 2 * L.sbo_by;
+      const uint64_t c_h = tc::desc(s_by + 0 * pl + kb, 128, L.sbo_by);
+      const uint64_t c_l = tc::desc(s_by + 1 * pl + kb, 128, L.sbo_by);
+      const uint64_t s_h = tc::desc(s_by + 2 * pl + kb, 128, L.sbo_by);
+      const uint64_t s_l = tc::desc(s_by + 3 * pl + kb, 128, L.sbo_by);
+      const uint32_t first = (yc == 0) ? 0u : 1u;
+#pragma unroll
+      for (int tile = 0; tile < 2; ++tile) {
+        const uint32_t a0 = s_ay + tile * kTileYBytes;
+        const uint64_t re_h = tc::desc(a0 + 0 * kTileYBytes, kLboY, kSboY);
+        const uint64_t re_l = tc::desc(a0 + 2 * kTileYBytes, kLboY, kSboY);
+        const uint64_t im_h = tc::desc(a0 + 4 * kTileYBytes, kLboY, kSboY);
+        const uint64_t im_l = tc::desc(a0 + 6 * kTileYBytes, kLboY, kSboY);
+        const uint32_t dre = d3 + 32 * tile, dim = dre + 16;
+        mma3(dre, re_h, re_l, c_h, c_l, id16, first);
+        mma3(dre, im_h, im_l, s_h, s_l, id16, 1u);
+        mma3(dim, im_h, im_l, c_h, c_l, id16, first);
+        mma3(dim, re_h, re_l, s_h, s_l, id16n, 1u);
+      }
+      tc::commit(&bar_y);
+    }
+    y_pending = true;
+    if (yc != n_yc - 1) continue;
+
+    // ---- slab epilogue: D3 -> XK exchange layout
+    tc::mbar_wait(&bar_y, ph_y);
+    ph_y ^= 1;
+    y_pending = false;
+    tc::fence_after();
+    {
+      const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+      float v[32];
+      tc::tmem_ld32(d3 + ((uint32_t)(32 * quarter) << 16) + 32 * part, v);
+      const int m = 32 * quarter + lane, kz = 8 * part + (m >> 4), kt = m & 15;
+      if (kz < g.rz && kt < g.rt) {
+#pragma unroll
+        for (int ky = 0; ky < 16; ++ky)
+          if (ky < g.ry)
+            out[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt] = make_float2(scale * v[ky], scale * v[16 + ky]);
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+  }
+  tc::cp_wait<0>();
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kFwdTmemCols>(tmem);
+}
+
+// ===========================================================================
+// inverse
+// ===========================================================================
+struct InvLayout {
+  int NY16, NZ16, KT, sbo_by, sbo_bz, sbo_bt;
+  int off_v, off_azt, off_by, off_bz, off_bt, total;
+};
+
+__host__ __device__ inline InvLayout inv_layout(int ny, int nz, int nt) {
+  InvLayout L;
+  L.NY16 = rup(ny, 16);
+  L.NZ16 = rup(nz, 16);
+  L.KT = rup(nt, kTileT);
+  int o = 0;
+  L.off_v = o;   o += 8 * kTile16;                // V: (re, im) x (hi, lo) x 2 tiles
+  L.off_azt = o; o += 8 * kTile16;                // A_Z' then A_T' (aliased)
+  L.off_by = o;  o += 4 * (L.NY16 / 8) * kBSbo16;  // rows y, K = ky
+  L.off_bz = o;  o += 4 * (L.NZ16 / 8) * kBSbo16;  // rows z, K = kz
+  L.off_bt = o;  o += 4 * (L.KT / 8) * kBSbo16;    // rows t, K = kt
+  L.total = o;
+  return L;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, const float2* __restrict__ in,
+                                                            float scale, float* __restrict__ out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
+  const int XL = x_local(g);
+  const InvLayout L = inv_layout(Ny, Nz, Nt);
+  unsigned char* av = smem + L.off_v;
+  unsigned char* azt = smem + L.off_azt;
+  unsigned char* by = smem + L.off_by;
+  unsigned char* bz = smem + L.off_bz;
+  unsigned char* bt = smem + L.off_bt;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, part = warp >> 2;
+
+  fill_cs(by, L.NY16, 16, kBSbo16, [&](int y, int k, double& c, double& s) {
+    if (y < Ny && k < g.ry) sincos_idx(mode_freq(k, Ny, g.my), y, Ny, s, c);
+  });
+  fill_cs(bz, L.NZ16, 16, kBSbo16, [&](int z, int k, double& c, double& s) {
+    if (z < Nz && k < g.rz) sincos_idx(mode_freq(k, Nz, g.mz), z, Nz, s, c);
+  });
+  fill_cs(bt, L.KT, 16, kBSbo16, [&](int t, int k, double& c, double& s) {
+    if (t < Nt && k < g.rt) sincos_idx(mode_freq(k, Nt, g.mt), t, Nt, s, c);
+  });
+  if (warp == 0) tc::tmem_alloc<kInvTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t d1 = tmem, d2 = tmem + 64, d3 = tmem + 320;
+  uint32_t ph = 0;
+  auto mma_done = [&]() {
+    tc::mbar_wait(&bar, ph);
+    ph ^= 1;
+    tc::fence_after();
+  };
+  const uint32_t id16 = tc::idesc_tf32(128, 16), id16n = tc::idesc_tf32(128, 16, false, true);
+  const uint32_t id32 = tc::idesc_tf32(128, 32), id32n = tc::idesc_tf32(128, 32, false, true);
+  const uint32_t s_av = tc::smem_u32(av), s_azt = tc::smem_u32(azt);
+  const uint32_t s_by = tc::smem_u32(by), s_bz = tc::smem_u32(bz), s_bt = tc::smem_u32(bt);
+  const uint32_t pl_by = (L.NY16 / 8) * kBSbo16, pl_bz = (L.NZ16 / 8) * kBSbo16, pl_bt = (L.KT / 8) * kBSbo16;
+  const int slabs = g.batch * g.c * XL;
+  const int n_yc = (Ny + 15) / 16, n_zc = (Nz + 63) / 64, n_tb = L.KT / kTileT;
+  const bool vec_out = (Nt % 4 == 0) && (((uintptr_t)out & 15) == 0);
+  const long long plane = (long long)Nz * Nt;
+
+  for (int slab = blockIdx.x; slab < slabs; slab += gridDim.x) {
+    const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+    float* o_slab = out + (((long long)bb * g.c + ch) * XL + xl) * (long long)Ny * plane;
+    // ---- V (XK layout) -> stage-Y' operand: row (kz % 8, kt) of tile kz / 8, k = ky
+    __syncthreads();  // previous slab's MMAs finished reading V (waited below)
+    for (int e = tid; e < 16 * 16 * 16; e += kThreads) {
+      const int ky = e >> 8, kz = (e >> 4) & 15, kt = e & 15;
+      float2 v = make_float2(0.f, 0.f);
+      if (ky < g.ry && kz < g.rz && kt < g.rt) v = in[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt];
+      const int off = (kz >> 3) * kTile16 + kmaj((kz & 7) * 16 + kt, ky, 128, kSbo16);
+      st_split(av + 0 * kTile16, av + 2 * kTile16, off, v.x);
+      st_split(av + 4 * kTile16, av + 6 * kTile16, off, v.y);
+    }
+    for (int yc = 0; yc < n_yc; ++yc) {
+      for (int zc = 0; zc < n_zc; ++zc) {
+        const int nz_c = min(64, L.NZ16 - 64 * zc);
+        tc::fence_proxy_async();
+        tc::fence_before();
+        __syncthreads();
+        // ---- stage Y': D1[tile][(kz%8,kt)][y] = sum_ky V e^{+i ky y}
+        if (tid == 0) {
+          tc::fence_after();
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const uint32_t kb = (uint32_t)(yc * 2) * kBSbo16 + 2 * s * 128;
+            const uint64_t c_h = tc::desc(s_by + 0 * pl_by + kb, 128, kBSbo16);
+            const uint64_t c_l = tc::desc(s_by + 1 * pl_by + kb, 128, kBSbo16);
+            const uint64_t s_h = tc::desc(s_by + 2 * pl_by + kb, 128, kBSbo16);
+            const uint64_t s_l = tc::desc(s_by + 3 * pl_by + kb, 128, kBSbo16);
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+              const uint32_t a0 = s_av + tile * kTile16 + 2 * s * 128;
+              const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
+              const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
+              const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
+              const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
+              const uint32_t dre = d1 + 32 * tile, dim = dre + 16, acc = s ? 1u : 0u;
+              // e^{+i}: re = A_re C - A_im S ; im = A_im C + A_re S
+              mma3(dre, re_h, re_l, c_h, c_l, id16, acc);
+              mma3(dre, im_h, im_l, s_h, s_l, id16n, 1u);
+              mma3(dim, im_h, im_l, c_h, c_l, id16, acc);
+              mma3(dim, re_h, re_l, s_h, s_l, id16, 1u);
+            }
+          }
+          tc::commit(&bar);
+        }
+        mma_done();
+        // ---- D1 -> A_Z': row (y % 8, kt) of tile y / 8, k = kz
+        {
+          float v[32];
+          const int tile = part;  // D1 tile = kz / 8
+          tc::tmem_ld32(d1 + ((uint32_t)(32 * quarter) << 16) + 32 * tile, v);
+          const int m = 32 * quarter + lane, kz = 8 * tile + (m >> 4), kt = m & 15;
+#pragma unroll
+          for (int y = 0; y < 16; ++y) {
+            const int off = (y >> 3) * kTile16 + kmaj((y & 7) * 16 + kt, kz, 128, kSbo16);
+            st_split(azt + 0 * kTile16, azt + 2 * kTile16, off, v[y]);
+            st_split(azt + 4 * kTile16, azt + 6 * kTile16, off, v[16 + y]);
+          }
+        }
+        tc::fence_proxy_async();
+        tc::fence_before();
+        __syncthreads();
+        // ---- stage Z': D2[tile][(y%8,kt)][z] = sum_kz D1 e^{+i kz z}, z in chunk zc
+        if (tid == 0) {
+          tc::fence_after();
+          const uint32_t idn = tc::idesc_tf32(128, nz_c), idnn = tc::idesc_tf32(128, nz_c, false, true);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const uint32_t kb = (uint32_t)(zc * 8) * kBSbo16 + 2 * s * 128;
+            const uint64_t c_h = tc::desc(s_bz + 0 * pl_bz + kb, 128, kBSbo16);
+            const uint64_t c_l = tc::desc(s_bz + 1 * pl_bz + kb, 128, kBSbo16);
+            const uint64_t s_h = tc::desc(s_bz + 2 * pl_bz + kb, 128, kBSbo16);
+            const uint64_t s_l = tc::desc(s_bz + 3 * pl_bz + kb, 128, kBSbo16);
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+              const uint32_t a0 = s_azt + tile * kTile16 + 2 * s * 128;
+              const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
+              const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
+              const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
+              const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
+              const uint32_t dre = d2 + 128 * tile, dim = dre + 64, acc = s ? 1u : 0u;
+              mma3(dre, re_h, re_l, c_h, c_l, idn, acc);
+              mma3(dre, im_h, im_l, s_h, s_l, idnn, 1u);
+              mma3(dim, im_h, im_l, c_h, c_l, idn, acc);
+              mma3(dim, re_h, re_l, s_h, s_l, idn, 1u);
+            }
+          }
+          tc::commit(&bar);
+        }
+        mma_done();
+        for (int zb = 0; zb < nz_c / 16; ++zb) {
+          // ---- D2 -> A_T': row (y % 8, zl) of tile y / 8, k = kt  (A_Z' no longer needed)
+          {
+            float re[16], im[16];
+            const int tile = part;  // D2 tile = y / 8
+            const uint32_t a = d2 + ((uint32_t)(32 * quarter) << 16) + 128 * tile + 16 * zb;
+            tc::tmem_ld16(a, re);
+            tc::tmem_ld16(a + 64, im);
+            const int m = 32 * quarter + lane, y8 = m >> 4, kt = m & 15;
+#pragma unroll
+            for (int zl = 0; zl < 16; ++zl) {
+              const int off = tile * kTile16 + kmaj(y8 * 16 + zl, kt, 128, kSbo16);
+              st_split(azt + 0 * kTile16, azt + 2 * kTile16, off, re[zl]);
+              st_split(azt + 4 * kTile16, azt + 6 * kTile16, off, im[zl]);
+            }
+          }
+          tc::fence_proxy_async();
+          tc::fence_before();
+          __syncthreads();
+          for (int tb = 0; tb < n_tb; ++tb) {
+            // ---- stage T': D3[tile][(y%8, zl)][t] = sum_kt (D2_re C - D2_im S)
+            if (tid == 0) {
+              tc::fence_after();
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                const uint32_t kb = (uint32_t)(tb * 4) * kBSbo16 + 2 * s * 128;
+                const uint64_t c_h = tc::desc(s_bt + 0 * pl_bt + kb, 128, kBSbo16);
+                const uint64_t c_l = tc::desc(s_bt + 1 * pl_bt + kb, 128, kBSbo16);
+                const uint64_t s_h = tc::desc(s_bt + 2 * pl_bt + kb, 128, kBSbo16);
+                const uint64_t s_l = tc::desc(s_bt + 3 * pl_bt + kb, 128, kBSbo16);
+#pragma unroll
+                for (int tile = 0; tile < 2; ++tile) {
+                  const uint32_t a0 = s_azt + tile * kTile16 + 2 * s * 128;
+                  const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
+                  const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
+                  const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
+                  const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
+                  const uint32_t d = d3 + 32 * tile;
+                  mma3(d, re_h, re_l, c_h, c_l, id32, s ? 1u : 0u);
+                  mma3(d, im_h, im_l, s_h, s_l, id32n, 1u);
+                }
+              }
+              tc::commit(&bar);
+            }
+            mma_done();
+            // ---- D3 -> output rows (y, z), 32 t each
+            {
+              float v[32];
+              const int tile = part;
+              tc::tmem_ld32(d3 + ((uint32_t)(32 * quarter) << 16) + 32 * tile, v);
+              const int m = 32 * quarter + lane;
+              const int y = yc * 16 + tile * 8 + (m >> 4), z = zc * 64 + zb * 16 + (m & 15);
+              const int t0 = tb * kTileT;
+              if (y < Ny && z < Nz) {
+                float* row = o_slab + (long long)y * plane + (long long)z * Nt + t0;
+                if (vec_out && t0 + kTileT <= Nt) {
+#pragma unroll
+                  for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<float4*>(row + 4 * q) =
+                        make_float4(scale * v[4 * q], scale * v[4 * q + 1], scale * v[4 * q + 2], scale * v[4 * q + 3]);
+                } else {
+#pragma unroll
+                  for (int t = 0; t < 32; ++t)
+                    if (t0 + t < Nt) row[t] = scale * v[t];
+                }
+              }
+            }
+            tc::fence_before();
+            __syncthreads();
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kInvTmemCols>(tmem);
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static bool supported(const dfno_geom& g) {
+  return g.dtype == DFNO_F32 && g.ry <= 16 && g.rz <= 16 && g.rt <= 16;
+}
+
+static constexpr int kSmemCap = 225 * 1024;
+
+template <int MODE, bool VEC, int STAGES>
+static int launch_fwd_s(const dfno_geom& g, const void* src, const void* pre, double scale, void* out,
+                        cudaStream_t st) {
+  const FwdLayout L = fwd_layout(g.ny, g.nz, g.nt, STAGES, MODE == DFNO_SRC_GRAD);
+  const size_t smem = (size_t)L.total;
+  auto kern = k_yzt_fwd_tc<MODE, VEC, STAGES>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  const int slabs = g.batch * g.c * x_local(g);
+  const int grid = sm_count() < slabs ? sm_count() : slabs;
+  kern<<<grid, kThreads, smem, st>>>(g, (const float*)src, (const float*)pre, (float)scale, (float2*)out);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+template <int MODE, bool VEC>
+static int launch_fwd(const dfno_geom& g, const void* src, const void* pre, double scale, void* out,
+                      cudaStream_t st) {
+  const bool grad = MODE == DFNO_SRC_GRAD;
+  if (fwd_layout(g.ny, g.nz, g.nt, 5, grad).total <= kSmemCap)
+    return launch_fwd_s<MODE, VEC, 5>(g, src, pre, scale, out, st);
+  if (fwd_layout(g.ny, g.nz, g.nt, 4, grad).total <= kSmemCap)
+    return launch_fwd_s<MODE, VEC, 4>(g, src, pre, scale, out, st);
+  if (fwd_layout(g.ny, g.nz, g.nt, 3, grad).total <= kSmemCap)
+    return launch_fwd_s<MODE, VEC, 3>(g, src, pre, scale, out, st);
+  if (fwd_layout(g.ny, g.nz, g.nt, 2, grad).total <= kSmemCap)
+    return launch_fwd_s<MODE, VEC, 2>(g, src, pre, scale, out, st);
   return DFNO_ERR_UNSUPPORTED;
 }
-int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t) { return DFNO_ERR_UNSUPPORTED; }
+
+int yzt_fwd_tc(const dfno_geom& g, const void* src, const void* pre, int mode, double scale, void* out,
+               cudaStream_t st) {
+  if (!supported(g)) return DFNO_ERR_UNSUPPORTED;
+  const bool vec = (g.nt % 4 == 0) && ((uintptr_t)src % 16 == 0) && (pre == nullptr || (uintptr_t)pre % 16 == 0);
+  switch (mode) {
+    case DFNO_SRC_ACT:
+      return vec ? launch_fwd<DFNO_SRC_ACT, true>(g, src, pre, scale, out, st)
+                 : launch_fwd<DFNO_SRC_ACT, false>(g, src, pre, scale, out, st);
+    case DFNO_SRC_GRAD:
+      return vec ? launch_fwd<DFNO_SRC_GRAD, true>(g, src, pre, scale, out, st)
+                 : launch_fwd<DFNO_SRC_GRAD, false>(g, src, pre, scale, out, st);
+    default:
+      return vec ? launch_fwd<DFNO_SRC_RAW, true>(g, src, pre, scale, out, st)
+                 : launch_fwd<DFNO_SRC_RAW, false>(g, src, pre, scale, out, st);
+  }
+}
+
+int yzt_inv_tc(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
+  if (!supported(g)) return DFNO_ERR_UNSUPPORTED;
+  const InvLayout L = inv_layout(g.ny, g.nz, g.nt);
+  if (L.total > kSmemCap) return DFNO_ERR_UNSUPPORTED;
+  if (cudaFuncSetAttribute(k_yzt_inv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  const int slabs = g.batch * g.c * x_local(g);
+  const int grid = sm_count() < slabs ? sm_count() : slabs;
+  k_yzt_inv_tc<<<grid, kThreads, L.total, st>>>(g, (const float2*)in, (float)scale, (float*)out);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
 }  // namespace dfno

@@ -33,7 +33,8 @@ def call(name, *args):
 
 
 def tol(dtype):
-    return 1e-12 if dtype == _lib.F64 else 2e-6
+    # fp32: SIMT fp32 or tcgen05 3xTF32 (round-to-nearest split, ~2^-22 per product)
+    return 1e-12 if dtype == _lib.F64 else 5e-6
 
 
 SHAPES = [((4, 64, 64, 32), (8, 8, 8, 8)), ((3, 32, 32, 16), (8, 8, 8, 8)), ((2, 30, 20, 22), (4, 8, 8, 8)),
@@ -63,7 +64,7 @@ def test_yzt_forward(grid, modes, dtype, mode):
     elif mode == _lib.SRC_GRAD:
         a64 = a64 * O.act_grad("gelu", pr.double().cpu().numpy())
     want = scale * O.yzt_truncated(a64, modes)
-    assert O.rel_err(out.cpu().numpy(), want) < tol(dtype) * (10 if mode != _lib.SRC_RAW else 1)
+    assert O.rel_err(out.cpu().numpy(), want) < tol(dtype) * (4 if mode != _lib.SRC_RAW else 1)
 
 
 @pytest.mark.parametrize("grid,modes", SHAPES)
