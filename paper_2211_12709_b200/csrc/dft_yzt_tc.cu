@@ -30,6 +30,8 @@
 //
 // Envelope: r_y, r_z, r_t <= 16 (m <= 8 per dim -- every BASELINE config);
 // other geometries use the SIMT kernels (dft_yzt.cu).
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -49,7 +51,7 @@ constexpr int kATRegion = (2 * kATBytes > kAYBytes) ? 2 * kATBytes : kAYBytes;  
 // inverse operand tiles: 128 rows x K = 16, LBO 128, SBO 528
 constexpr int kSbo16 = 528, kTile16 = 16 * kSbo16;
 constexpr int kBSbo16 = 512;                       // twiddle B with K = 16
-constexpr uint32_t kFwdTmemCols = 128, kInvTmemCols = 512;
+constexpr uint32_t kFwdTmemCols = 256, kInvTmemCols = 512;
 
 __host__ __device__ inline int rup(int a, int b) { return (a + b - 1) / b * b; }
 
@@ -112,11 +114,11 @@ __device__ __forceinline__ void mma3(uint32_t d, uint64_t a_hi, uint64_t a_lo, u
 }
 
 struct FwdLayout {
-  int KT, NZ16, NY8, sbo_bt, sbo_bz, sbo_by, stages, stage_bytes;
-  int off_raw, off_at, off_az, off_bt, off_bz, off_by, total;
+  int KT, NZ16, NY8, sbo_bt, sbo_bz, sbo_by;
+  int off_at, off_az, off_ay, off_bt, off_bz, off_by, total;
 };
 
-__host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt, int stages, bool grad) {
+__host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt) {
   FwdLayout L;
   L.KT = rup(nt, kTileT);
   L.NZ16 = rup(nz, 16);
@@ -124,42 +126,62 @@ __host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt, int stag
   L.sbo_bt = (L.KT / 4) * 128;
   L.sbo_bz = (L.NZ16 / 4) * 128;
   L.sbo_by = (L.NY8 / 4) * 128;
-  L.stages = stages;
-  L.stage_bytes = kRawBytes * (grad ? 2 : 1);
   int o = 0;
-  L.off_raw = o; o += stages * L.stage_bytes;
-  L.off_at = o;  o += kATRegion;
-  L.off_az = o;  o += 4 * kAZBytes;
-  L.off_bt = o;  o += 2 * 4 * L.sbo_bt;
-  L.off_bz = o;  o += 4 * 2 * L.sbo_bz;
-  L.off_by = o;  o += 4 * 2 * L.sbo_by;
+  L.off_at = o; o += 2 * kATBytes;
+  L.off_az = o; o += 4 * kAZBytes;
+  L.off_ay = o; o += kAYBytes;
+  L.off_bt = o; o += 2 * 4 * L.sbo_bt;
+  L.off_bz = o; o += 4 * 2 * L.sbo_bz;
+  L.off_by = o; o += 4 * 2 * L.sbo_by;
   L.total = o;
   return L;
 }
+
+// Walks the tiles (slab, y chunk, z block, t block) of one CTA in order
+// without divisions in the steady state.
+struct TileCursor {
+  int slab, yc, zb, tb;
+  long long base;  // element offset of the slab
+  __device__ void set_slab(const dfno_geom& g, int s, int XL, long long slab_elems) {
+    slab = s;
+    base = (long long)s * slab_elems;  // slabs are contiguous (b, c, x) in the activation layout
+    (void)g;
+    (void)XL;
+  }
+  __device__ void advance(const dfno_geom& g, int n_yc, int n_zb, int n_tb, int XL, long long slab_elems) {
+    if (++tb < n_tb) return;
+    tb = 0;
+    if (++zb < n_zb) return;
+    zb = 0;
+    if (++yc < n_yc) return;
+    yc = 0;
+    set_slab(g, slab + (int)gridDim.x, XL, slab_elems);
+  }
+};
 
 }  // namespace
 
 // ===========================================================================
 // forward
 // ===========================================================================
-template <int MODE, bool VEC, int STAGES>
+template <int MODE, bool VEC, int PF>
 __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, const float* __restrict__ src,
                                                             const float* __restrict__ pre, float scale,
                                                             float2* __restrict__ out) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
-  constexpr int D = STAGES - 1;  // prefetch distance (tiles in flight)
+  constexpr int NV = VEC ? 4 : 16;  // loads per thread per tile (float4 or float)
+  using LT = typename std::conditional<VEC, float4, float>::type;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar_t, bar_z, bar_y;
   __shared__ uint32_t tmem_base;
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
-  const FwdLayout L = fwd_layout(Ny, Nz, Nt, STAGES, GRAD);
-  unsigned char* raw = smem + L.off_raw;
+  const FwdLayout L = fwd_layout(Ny, Nz, Nt);
   unsigned char* at_hi = smem + L.off_at;
   unsigned char* at_lo = at_hi + kATBytes;
-  unsigned char* ay = smem + L.off_at;  // aliases A_T (used after the last stage-T of a chunk)
   unsigned char* az = smem + L.off_az;
+  unsigned char* ay = smem + L.off_ay;
   unsigned char* bt = smem + L.off_bt;
   unsigned char* bz = smem + L.off_bz;
   unsigned char* by = smem + L.off_by;
@@ -197,14 +219,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  const uint32_t d1 = tmem, d2 = tmem + 32, d3 = tmem + 64;
+  const uint32_t d2 = tmem + 64, d3 = tmem + 96;  // D1 double buffer at 0 / 32
 
   const int n_yc = (Ny + 7) / 8, n_zb = (Nz + 15) / 16, n_tb = L.KT / kTileT;
-  const int tiles_per_slab = n_yc * n_zb * n_tb;
   const int slabs = g.batch * g.c * XL;
   const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int total = my_slabs * tiles_per_slab;
+  const int total = my_slabs * n_yc * n_zb * n_tb;
   const long long plane = (long long)Nz * Nt;
+  const long long slab_elems = (long long)Ny * plane;
   const int quarter = warp & 3, part = warp >> 2;
 
   const uint32_t id_t = tc::idesc_tf32(128, 32);
@@ -214,128 +236,85 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
   const uint32_t s_az = tc::smem_u32(az), s_ay = tc::smem_u32(ay);
   const uint32_t s_bt = tc::smem_u32(bt), s_bz = tc::smem_u32(bz), s_by = tc::smem_u32(by);
 
-  // tile i -> (slab, yc, zb, tb)
-  auto coords = [&](int i, int& slab, int& yc, int& zb, int& tb) {
-    const int sl = i / tiles_per_slab, r = i % tiles_per_slab;
-    slab = (int)blockIdx.x + sl * (int)gridDim.x;
-    yc = r / (n_zb * n_tb);
-    zb = (r / n_tb) % n_zb;
-    tb = r % n_tb;
-  };
-  auto slab_base = [&](int slab) -> long long {
-    const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
-    return (((long long)bb * g.c + ch) * XL + xl) * (long long)Ny * plane;
-  };
-  // issue the cp.async copies of tile i into its ring stage
-  auto issue = [&](int i) {
-    if (i < total) {
-      int slab, yc, zb, tb;
-      coords(i, slab, yc, zb, tb);
-      const long long sb = slab_base(slab);
-      unsigned char* st = raw + (i % STAGES) * L.stage_bytes;
-      const int y0 = yc * 8, z0 = zb * 16, t0 = tb * kTileT;
-      if (VEC) {
+  // per-thread tile geometry (tile rows = (y, z) = 8 x 16, 32 t):
+  //   VEC    : row = (tid >> 3) + 32 j -> y = (tid >> 7) + 2 j, z = (tid >> 3) & 15, t = 4 (tid & 7)
+  //   scalar : row = (tid >> 5) + 8 j  -> y = j >> 1, z = (tid >> 5) + 8 (j & 1),    t = tid & 31
+  const int tt = VEC ? 4 * (tid & 7) : (tid & 31);
+
+  LT buf[PF][NV];
+  LT pbuf[GRAD ? PF : 1][GRAD ? NV : 1];
+
+  auto load_tile = [&](const TileCursor& c, LT (&b)[NV], LT (&pb)[GRAD ? NV : 1]) {
+    const int y0 = c.yc * 8, z0 = c.zb * 16, t = c.tb * kTileT + tt;
+    const bool t_ok = t < Nt;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int q = tid + kThreads * j, row = q >> 3, c4 = q & 7;
-          const int y = y0 + (row >> 4), z = z0 + (row & 15), t = t0 + 4 * c4;
-          const bool ok = (y < Ny) && (z < Nz) && (t < Nt);
-          const long long go = ok ? sb + (long long)y * plane + (long long)z * Nt + t : sb;
-          tc::cp16(st + row * 128 + c4 * 16, src + go, ok);
-          if (GRAD) tc::cp16(st + kRawBytes + row * 128 + c4 * 16, pre + go, ok);
-        }
+    for (int j = 0; j < NV; ++j) {
+      const int y = VEC ? y0 + (tid >> 7) + 2 * j : y0 + (j >> 1);
+      const int z = VEC ? z0 + ((tid >> 3) & 15) : z0 + (tid >> 5) + 8 * (j & 1);
+      const bool ok = t_ok && (z < Nz) && (y < Ny);
+      const long long off = c.base + (long long)y * plane + (long long)z * Nt + t;
+      if constexpr (VEC) {
+        b[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (GRAD)
+          pb[j] = ok ? __ldg(reinterpret_cast<const float4*>(pre + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          const int e = tid + kThreads * j, row = e >> 5, tt = e & 31;
-          const int y = y0 + (row >> 4), z = z0 + (row & 15), t = t0 + tt;
-          const bool ok = (y < Ny) && (z < Nz) && (t < Nt);
-          const long long go = ok ? sb + (long long)y * plane + (long long)z * Nt + t : sb;
-          tc::cp4(st + row * 128 + tt * 4, src + go, ok);
-          if (GRAD) tc::cp4(st + kRawBytes + row * 128 + tt * 4, pre + go, ok);
-        }
+        b[j] = ok ? __ldg(src + off) : 0.f;
+        if constexpr (GRAD) pb[j] = ok ? __ldg(pre + off) : 0.f;
       }
     }
-    tc::cp_commit();
   };
+  auto convert_tile = [&](LT (&b)[NV], LT (&pb)[GRAD ? NV : 1]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if constexpr (VEC) {
+        float4 v = b[j];
+        float4 p = GRAD ? pb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v.x = transform<MODE>(v.x, p.x, g.act);
+        v.y = transform<MODE>(v.y, p.y, g.act);
+        v.z = transform<MODE>(v.z, p.z, g.act);
+        v.w = transform<MODE>(v.w, p.w, g.act);
+        float4 h, l;
+        tc::split_hl(v.x, h.x, l.x);
+        tc::split_hl(v.y, h.y, l.y);
+        tc::split_hl(v.z, h.z, l.z);
+        tc::split_hl(v.w, h.w, l.w);
+        const int row = (tid >> 3) + 32 * j;
+        const int off = (row >> 3) * kSboT + (tid & 7) * kLboT + (row & 7) * 16;
+        *reinterpret_cast<float4*>(at_hi + off) = h;
+        *reinterpret_cast<float4*>(at_lo + off) = l;
+      } else {
+        const float v = transform<MODE>(b[j], GRAD ? pb[j] : 0.f, g.act);
+        const int row = (tid >> 5) + 8 * j;
+        float h, l;
+        tc::split_hl(v, h, l);
+        const int off = kmaj(row, tid & 31, kLboT, kSboT);
+        *reinterpret_cast<float*>(at_hi + off) = h;
+        *reinterpret_cast<float*>(at_lo + off) = l;
+      }
+    }
+  };
+
+  TileCursor lc, pc;
+  lc.yc = lc.zb = lc.tb = 0;
+  lc.set_slab(g, blockIdx.x, XL, slab_elems);
+  pc = lc;
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    if (k < total) {
+      if constexpr (GRAD) load_tile(lc, buf[k], pbuf[k]);
+      else load_tile(lc, buf[k], pbuf[0]);
+      lc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
+    }
+  }
 
   uint32_t ph_t = 0, ph_z = 0, ph_y = 0;
-  bool t_pending = false, z_pending = false, y_pending = false;
-#pragma unroll 1
-  for (int p = 0; p < D; ++p) issue(p);
+  bool z_pending = false, y_pending = false;
+  int group = 0;  // (y chunk, z block) group counter -> D1 buffer parity
+  TileCursor ec;  // cursor of the group awaiting its epilogue
+  bool ep_pending = false;
 
-#pragma unroll 1
-  for (int i = 0; i < total; ++i) {
-    int slab, yc, zb, tb;
-    coords(i, slab, yc, zb, tb);
-    issue(i + D);
-    tc::cp_wait<D>();
-    // A_T / A_Y must be free: stage-T of the previous tile and stage-Y of the previous chunk done
-    if (t_pending) {
-      tc::mbar_wait(&bar_t, ph_t);
-      ph_t ^= 1;
-      t_pending = false;
-    }
-    if (y_pending) {
-      tc::mbar_wait(&bar_y, ph_y);
-      ph_y ^= 1;
-      y_pending = false;
-    }
-    // ---- convert the staged raw tile into the stage-T operand (hi / lo)
-    {
-      const unsigned char* st = raw + (i % STAGES) * L.stage_bytes;
-      if (VEC) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int q = tid + kThreads * j, row = q >> 3, c4 = q & 7;
-          float4 v = *reinterpret_cast<const float4*>(st + row * 128 + c4 * 16);
-          float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (GRAD) p = *reinterpret_cast<const float4*>(st + kRawBytes + row * 128 + c4 * 16);
-          v.x = transform<MODE>(v.x, p.x, g.act);
-          v.y = transform<MODE>(v.y, p.y, g.act);
-          v.z = transform<MODE>(v.z, p.z, g.act);
-          v.w = transform<MODE>(v.w, p.w, g.act);
-          float4 h, l;
-          tc::split_rn(v.x, h.x, l.x);
-          tc::split_rn(v.y, h.y, l.y);
-          tc::split_rn(v.z, h.z, l.z);
-          tc::split_rn(v.w, h.w, l.w);
-          const int off = (row >> 3) * kSboT + c4 * kLboT + (row & 7) * 16;
-          *reinterpret_cast<float4*>(at_hi + off) = h;
-          *reinterpret_cast<float4*>(at_lo + off) = l;
-        }
-      } else {
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          const int e = tid + kThreads * j, row = e >> 5, tt = e & 31;
-          float v = *reinterpret_cast<const float*>(st + row * 128 + tt * 4);
-          const float p = GRAD ? *reinterpret_cast<const float*>(st + kRawBytes + row * 128 + tt * 4) : 0.f;
-          st_split(at_hi, at_lo, kmaj(row, tt, kLboT, kSboT), transform<MODE>(v, p, g.act));
-        }
-      }
-    }
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    // ---- stage T
-    if (tid == 0) {
-      tc::fence_after();
-#pragma unroll
-      for (int s = 0; s < kTileT / 8; ++s) {
-        const uint32_t ka = 2 * s * kLboT, kb = (uint32_t)(tb * (kTileT / 4) + 2 * s) * 128;
-        mma3(d1, tc::desc(s_at_hi + ka, kLboT, kSboT), tc::desc(s_at_lo + ka, kLboT, kSboT),
-             tc::desc(s_bt + kb, 128, L.sbo_bt), tc::desc(s_bt + 4 * L.sbo_bt + kb, 128, L.sbo_bt), id_t,
-             (tb > 0 || s > 0) ? 1u : 0u);
-      }
-      tc::commit(&bar_t);
-    }
-    t_pending = true;
-    if (tb != n_tb - 1) continue;
-
-    // ---- epilogue T -> A_Z (needs D1; A_Z released by the previous stage Z)
-    tc::mbar_wait(&bar_t, ph_t);
-    ph_t ^= 1;
-    t_pending = false;
+  // epilogue of a finished (yc, zb) group: D1 -> A_Z -> stage Z (+ chunk / slab ends)
+  auto epilogue = [&](const TileCursor& c, int grp) {
     if (z_pending) {
       tc::mbar_wait(&bar_z, ph_z);
       ph_z ^= 1;
@@ -344,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
     tc::fence_after();
     {
       float v[16];
-      tc::tmem_ld16(d1 + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
+      tc::tmem_ld16(tmem + 32 * (grp & 1) + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
       const int r = 32 * quarter + lane, y = r >> 4, zl = r & 15;  // D1 row = (y, zl)
       unsigned char* hi = az + part * 2 * kAZBytes;
       unsigned char* lo = hi + kAZBytes;
@@ -355,13 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
-    // ---- stage Z (K block zb = 16 z = 2 K steps), planar complex
     if (tid == 0) {
       tc::fence_after();
       const uint32_t pl = 2 * L.sbo_bz;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        const uint32_t ka = 2 * s * kLboZ, kb = (uint32_t)(zb * 4 + 2 * s) * 128;
+        const uint32_t ka = 2 * s * kLboZ, kb = (uint32_t)(c.zb * 4 + 2 * s) * 128;
         const uint64_t re_h = tc::desc(s_az + 0 * kAZBytes + ka, kLboZ, kSboZ);
         const uint64_t re_l = tc::desc(s_az + 1 * kAZBytes + ka, kLboZ, kSboZ);
         const uint64_t im_h = tc::desc(s_az + 2 * kAZBytes + ka, kLboZ, kSboZ);
@@ -370,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
         const uint64_t c_l = tc::desc(s_bz + 1 * pl + kb, 128, L.sbo_bz);
         const uint64_t s_h = tc::desc(s_bz + 2 * pl + kb, 128, L.sbo_bz);
         const uint64_t s_l = tc::desc(s_bz + 3 * pl + kb, 128, L.sbo_bz);
-        const uint32_t first = (zb == 0 && s == 0) ? 0u : 1u;
+        const uint32_t first = (c.zb == 0 && s == 0) ? 0u : 1u;
         // e^{-i}: re += A_re C + A_im S ;  im += A_im C - A_re S
         mma3(d2, re_h, re_l, c_h, c_l, id16, first);
         mma3(d2, im_h, im_l, s_h, s_l, id16, 1u);
@@ -380,12 +358,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
       tc::commit(&bar_z);
     }
     z_pending = true;
-    if (zb != n_zb - 1) continue;
-
-    // ---- epilogue Z -> A_Y (A_Y aliases A_T: stage T of this tile is done)
+    if (c.zb != n_zb - 1) return;
+    // ---- chunk end: D2 -> A_Y -> stage Y
     tc::mbar_wait(&bar_z, ph_z);
     ph_z ^= 1;
     z_pending = false;
+    if (y_pending) {
+      tc::mbar_wait(&bar_y, ph_y);
+      ph_y ^= 1;
+      y_pending = false;
+    }
     tc::fence_after();
     {
       float v[16];
@@ -401,15 +383,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
-    // ---- stage Y (K = the 8 y of chunk yc)
     if (tid == 0) {
       tc::fence_after();
-      const uint32_t kb = (uint32_t)(yc * 2) * 128, pl = 2 * L.sbo_by;
+      const uint32_t kb = (uint32_t)(c.yc * 2) * 128, pl = 2 * L.sbo_by;
       const uint64_t c_h = tc::desc(s_by + 0 * pl + kb, 128, L.sbo_by);
       const uint64_t c_l = tc::desc(s_by + 1 * pl + kb, 128, L.sbo_by);
       const uint64_t s_h = tc::desc(s_by + 2 * pl + kb, 128, L.sbo_by);
       const uint64_t s_l = tc::desc(s_by + 3 * pl + kb, 128, L.sbo_by);
-      const uint32_t first = (yc == 0) ? 0u : 1u;
+      const uint32_t first = (c.yc == 0) ? 0u : 1u;
 #pragma unroll
       for (int tile = 0; tile < 2; ++tile) {
         const uint32_t a0 = s_ay + tile * kTileYBytes;
@@ -426,15 +407,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
       tc::commit(&bar_y);
     }
     y_pending = true;
-    if (yc != n_yc - 1) continue;
-
-    // ---- slab epilogue: D3 -> XK exchange layout
+    if (c.yc != n_yc - 1) return;
+    // ---- slab end: D3 -> XK exchange layout
     tc::mbar_wait(&bar_y, ph_y);
     ph_y ^= 1;
     y_pending = false;
     tc::fence_after();
     {
-      const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+      const int slab = c.slab, xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
       float v[32];
       tc::tmem_ld32(d3 + ((uint32_t)(32 * quarter) << 16) + 32 * part, v);
       const int m = 32 * quarter + lane, kz = 8 * part + (m >> 4), kt = m & 15;
@@ -447,8 +427,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
     }
     tc::fence_before();
     __syncthreads();
+  };
+
+  // one tile: convert (prefetched registers) -> A_T, refill the registers,
+  // stage-T MMAs, then the lagging epilogue of the previous group
+  auto step = [&](LT (&b)[NV], LT (&pb)[GRAD ? NV : 1], int i) {
+    if (i > 0) {  // A_T free: stage T of the previous tile finished
+      tc::mbar_wait(&bar_t, ph_t);
+      ph_t ^= 1;
+    }
+    convert_tile(b, pb);
+    if (i + PF < total) {
+      load_tile(lc, b, pb);
+      lc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t dd = tmem + 32 * (group & 1);
+#pragma unroll
+      for (int s = 0; s < kTileT / 8; ++s) {
+        const uint32_t ka = 2 * s * kLboT, kb = (uint32_t)(pc.tb * (kTileT / 4) + 2 * s) * 128;
+        mma3(dd, tc::desc(s_at_hi + ka, kLboT, kSboT), tc::desc(s_at_lo + ka, kLboT, kSboT),
+             tc::desc(s_bt + kb, 128, L.sbo_bt), tc::desc(s_bt + 4 * L.sbo_bt + kb, 128, L.sbo_bt), id_t,
+             (pc.tb > 0 || s > 0) ? 1u : 0u);
+      }
+      tc::commit(&bar_t);
+    }
+    if (ep_pending) {
+      epilogue(ec, group - 1);
+      ep_pending = false;
+    }
+    if (pc.tb == n_tb - 1) {  // this group is complete once its last stage-T lands
+      ec = pc;
+      ep_pending = true;
+      ++group;
+    }
+    pc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
+  };
+
+#pragma unroll 1
+  for (int i0 = 0; i0 < total; i0 += PF) {
+#pragma unroll
+    for (int k = 0; k < PF; ++k) {
+      if (i0 + k < total) {
+        if constexpr (GRAD) step(buf[k], pbuf[k], i0 + k);
+        else step(buf[k], pbuf[0], i0 + k);
+      }
+    }
   }
-  tc::cp_wait<0>();
+  if (total > 0) {
+    tc::mbar_wait(&bar_t, ph_t);
+    ph_t ^= 1;
+    if (ep_pending) epilogue(ec, group - 1);
+  }
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<kFwdTmemCols>(tmem);
@@ -480,13 +514,15 @@ __host__ __device__ inline InvLayout inv_layout(int ny, int nz, int nt) {
 __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, const float2* __restrict__ in,
                                                             float scale, float* __restrict__ out) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;
+  // one barrier per D3 buffer: a commit is never outstanding twice on the
+  // same barrier when it is waited on (phase parity would alias)
+  __shared__ uint64_t bar_y, bar_z, bar_t[2];
   __shared__ uint32_t tmem_base;
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
   const InvLayout L = inv_layout(Ny, Nz, Nt);
   unsigned char* av = smem + L.off_v;
-  unsigned char* azt = smem + L.off_azt;
+  unsigned char* azt = smem + L.off_azt;  // A_Z' (2 tiles) -- later A_T' buffers 0 / 1 (1 tile each)
   unsigned char* by = smem + L.off_by;
   unsigned char* bz = smem + L.off_bz;
   unsigned char* bt = smem + L.off_bt;
@@ -504,7 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
   });
   if (warp == 0) tc::tmem_alloc<kInvTmemCols>(&tmem_base);
   if (tid == 0) {
-    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&bar_y, 1);
+    tc::mbar_init(&bar_z, 1);
+    tc::mbar_init(&bar_t[0], 1);
+    tc::mbar_init(&bar_t[1], 1);
     tc::mbar_fence_init();
   }
   tc::fence_proxy_async();
@@ -512,13 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  const uint32_t d1 = tmem, d2 = tmem + 64, d3 = tmem + 320;
-  uint32_t ph = 0;
-  auto mma_done = [&]() {
-    tc::mbar_wait(&bar, ph);
-    ph ^= 1;
-    tc::fence_after();
-  };
+  const uint32_t d1 = tmem, d2 = tmem + 64, d3 = tmem + 320;  // D3 double buffer at 320 / 352
+  uint32_t ph_y = 0, ph_z = 0, ph_t0 = 0, ph_t1 = 0;
   const uint32_t id16 = tc::idesc_tf32(128, 16), id16n = tc::idesc_tf32(128, 16, false, true);
   const uint32_t id32 = tc::idesc_tf32(128, 32), id32n = tc::idesc_tf32(128, 32, false, true);
   const uint32_t s_av = tc::smem_u32(av), s_azt = tc::smem_u32(azt);
@@ -529,11 +563,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
   const bool vec_out = (Nt % 4 == 0) && (((uintptr_t)out & 15) == 0);
   const long long plane = (long long)Nz * Nt;
 
+  // stage Y' for y chunk yc (reads V, writes D1)
+  auto issue_y = [&](int yc) {
+    if (tid != 0) return;
+    tc::fence_after();
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const uint32_t kb = (uint32_t)(yc * 2) * kBSbo16 + 2 * s * 128;
+      const uint64_t c_h = tc::desc(s_by + 0 * pl_by + kb, 128, kBSbo16);
+      const uint64_t c_l = tc::desc(s_by + 1 * pl_by + kb, 128, kBSbo16);
+      const uint64_t s_h = tc::desc(s_by + 2 * pl_by + kb, 128, kBSbo16);
+      const uint64_t s_l = tc::desc(s_by + 3 * pl_by + kb, 128, kBSbo16);
+#pragma unroll
+      for (int tile = 0; tile < 2; ++tile) {
+        const uint32_t a0 = s_av + tile * kTile16 + 2 * s * 128;
+        const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
+        const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
+        const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
+        const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
+        const uint32_t dre = d1 + 32 * tile, dim = dre + 16, acc = s ? 1u : 0u;
+        // e^{+i}: re = A_re C - A_im S ; im = A_im C + A_re S
+        mma3(dre, re_h, re_l, c_h, c_l, id16, acc);
+        mma3(dre, im_h, im_l, s_h, s_l, id16n, 1u);
+        mma3(dim, im_h, im_l, c_h, c_l, id16, acc);
+        mma3(dim, re_h, re_l, s_h, s_l, id16, 1u);
+      }
+    }
+    tc::commit(&bar_y);
+  };
+
   for (int slab = blockIdx.x; slab < slabs; slab += gridDim.x) {
     const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
     float* o_slab = out + (((long long)bb * g.c + ch) * XL + xl) * (long long)Ny * plane;
     // ---- V (XK layout) -> stage-Y' operand: row (kz % 8, kt) of tile kz / 8, k = ky
-    __syncthreads();  // previous slab's MMAs finished reading V (waited below)
     for (int e = tid; e < 16 * 16 * 16; e += kThreads) {
       const int ky = e >> 8, kz = (e >> 4) & 15, kt = e & 15;
       float2 v = make_float2(0.f, 0.f);
@@ -542,41 +604,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
       st_split(av + 0 * kTile16, av + 2 * kTile16, off, v.x);
       st_split(av + 4 * kTile16, av + 6 * kTile16, off, v.y);
     }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    issue_y(0);
     for (int yc = 0; yc < n_yc; ++yc) {
       for (int zc = 0; zc < n_zc; ++zc) {
         const int nz_c = min(64, L.NZ16 - 64 * zc);
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        // ---- stage Y': D1[tile][(kz%8,kt)][y] = sum_ky V e^{+i ky y}
-        if (tid == 0) {
-          tc::fence_after();
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const uint32_t kb = (uint32_t)(yc * 2) * kBSbo16 + 2 * s * 128;
-            const uint64_t c_h = tc::desc(s_by + 0 * pl_by + kb, 128, kBSbo16);
-            const uint64_t c_l = tc::desc(s_by + 1 * pl_by + kb, 128, kBSbo16);
-            const uint64_t s_h = tc::desc(s_by + 2 * pl_by + kb, 128, kBSbo16);
-            const uint64_t s_l = tc::desc(s_by + 3 * pl_by + kb, 128, kBSbo16);
-#pragma unroll
-            for (int tile = 0; tile < 2; ++tile) {
-              const uint32_t a0 = s_av + tile * kTile16 + 2 * s * 128;
-              const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
-              const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
-              const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
-              const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
-              const uint32_t dre = d1 + 32 * tile, dim = dre + 16, acc = s ? 1u : 0u;
-              // e^{+i}: re = A_re C - A_im S ; im = A_im C + A_re S
-              mma3(dre, re_h, re_l, c_h, c_l, id16, acc);
-              mma3(dre, im_h, im_l, s_h, s_l, id16n, 1u);
-              mma3(dim, im_h, im_l, c_h, c_l, id16, acc);
-              mma3(dim, re_h, re_l, s_h, s_l, id16, 1u);
-            }
-          }
-          tc::commit(&bar);
+        if (zc > 0) {  // recompute stage Y' for the next z chunk (D1 was consumed)
+          issue_y(yc);
         }
-        mma_done();
         // ---- D1 -> A_Z': row (y % 8, kt) of tile y / 8, k = kz
+        tc::mbar_wait(&bar_y, ph_y);
+        ph_y ^= 1;
+        tc::fence_after();
         {
           float v[32];
           const int tile = part;  // D1 tile = kz / 8
@@ -592,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
         tc::fence_proxy_async();
         tc::fence_before();
         __syncthreads();
-        // ---- stage Z': D2[tile][(y%8,kt)][z] = sum_kz D1 e^{+i kz z}, z in chunk zc
+        // ---- stage Z' (and, early, stage Y' of the next y chunk)
         if (tid == 0) {
           tc::fence_after();
           const uint32_t idn = tc::idesc_tf32(128, nz_c), idnn = tc::idesc_tf32(128, nz_c, false, true);
@@ -617,32 +658,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
               mma3(dim, re_h, re_l, s_h, s_l, idn, 1u);
             }
           }
-          tc::commit(&bar);
+          tc::commit(&bar_z);
         }
-        mma_done();
-        for (int zb = 0; zb < nz_c / 16; ++zb) {
-          // ---- D2 -> A_T': row (y % 8, zl) of tile y / 8, k = kt  (A_Z' no longer needed)
-          {
-            float re[16], im[16];
-            const int tile = part;  // D2 tile = y / 8
-            const uint32_t a = d2 + ((uint32_t)(32 * quarter) << 16) + 128 * tile + 16 * zb;
-            tc::tmem_ld16(a, re);
-            tc::tmem_ld16(a + 64, im);
-            const int m = 32 * quarter + lane, y8 = m >> 4, kt = m & 15;
+        if (zc == n_zc - 1 && yc + 1 < n_yc) issue_y(yc + 1);
+        tc::mbar_wait(&bar_z, ph_z);
+        ph_z ^= 1;
+        tc::fence_after();
+        // ---- stage T' steps over (z block, y tile, t block), software pipelined:
+        //      write A_T'[tile] -> MMA into D3[s & 1] -> store D3 of the previous step
+        const int n_steps = (nz_c / 16) * 2 * n_tb;
+        int prev_y = -1, prev_z = 0, prev_t0 = 0;
+        for (int st = 0; st <= n_steps; ++st) {
+          if (st < n_steps) {
+            const int tb = st % n_tb, tile = (st / n_tb) & 1, zb = st / (2 * n_tb);
+            if (tb == 0) {
+              // D2 (tile rows (y % 8, kt), cols z of block zb) -> A_T'[tile]: row (y % 8, zl), k = kt
+              float v[16];
+              const uint32_t a = d2 + ((uint32_t)(32 * quarter) << 16) + 128 * tile + 64 * part + 16 * zb;
+              tc::tmem_ld16(a, v);  // part 0: re, part 1: im
+              const int m = 32 * quarter + lane, y8 = m >> 4, kt = m & 15;
+              unsigned char* hi = azt + tile * 4 * kTile16 + part * 2 * kTile16;
+              unsigned char* lo = hi + kTile16;
 #pragma unroll
-            for (int zl = 0; zl < 16; ++zl) {
-              const int off = tile * kTile16 + kmaj(y8 * 16 + zl, kt, 128, kSbo16);
-              st_split(azt + 0 * kTile16, azt + 2 * kTile16, off, re[zl]);
-              st_split(azt + 4 * kTile16, azt + 6 * kTile16, off, im[zl]);
+              for (int zl = 0; zl < 16; ++zl) st_split(hi, lo, kmaj(y8 * 16 + zl, kt, 128, kSbo16), v[zl]);
+              tc::fence_proxy_async();
             }
-          }
-          tc::fence_proxy_async();
-          tc::fence_before();
-          __syncthreads();
-          for (int tb = 0; tb < n_tb; ++tb) {
-            // ---- stage T': D3[tile][(y%8, zl)][t] = sum_kt (D2_re C - D2_im S)
+            tc::fence_before();
+            __syncthreads();
             if (tid == 0) {
               tc::fence_after();
+              const uint32_t a0 = s_azt + tile * 4 * kTile16;
+              const uint32_t d = d3 + 32 * (st & 1);
 #pragma unroll
               for (int s = 0; s < 2; ++s) {
                 const uint32_t kb = (uint32_t)(tb * 4) * kBSbo16 + 2 * s * 128;
@@ -650,47 +696,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_inv_tc(const dfno_geom g, c
                 const uint64_t c_l = tc::desc(s_bt + 1 * pl_bt + kb, 128, kBSbo16);
                 const uint64_t s_h = tc::desc(s_bt + 2 * pl_bt + kb, 128, kBSbo16);
                 const uint64_t s_l = tc::desc(s_bt + 3 * pl_bt + kb, 128, kBSbo16);
-#pragma unroll
-                for (int tile = 0; tile < 2; ++tile) {
-                  const uint32_t a0 = s_azt + tile * kTile16 + 2 * s * 128;
-                  const uint64_t re_h = tc::desc(a0 + 0 * kTile16, 128, kSbo16);
-                  const uint64_t re_l = tc::desc(a0 + 2 * kTile16, 128, kSbo16);
-                  const uint64_t im_h = tc::desc(a0 + 4 * kTile16, 128, kSbo16);
-                  const uint64_t im_l = tc::desc(a0 + 6 * kTile16, 128, kSbo16);
-                  const uint32_t d = d3 + 32 * tile;
-                  mma3(d, re_h, re_l, c_h, c_l, id32, s ? 1u : 0u);
-                  mma3(d, im_h, im_l, s_h, s_l, id32n, 1u);
-                }
+                const uint64_t re_h = tc::desc(a0 + 0 * kTile16 + 2 * s * 128, 128, kSbo16);
+                const uint64_t re_l = tc::desc(a0 + 1 * kTile16 + 2 * s * 128, 128, kSbo16);
+                const uint64_t im_h = tc::desc(a0 + 2 * kTile16 + 2 * s * 128, 128, kSbo16);
+                const uint64_t im_l = tc::desc(a0 + 3 * kTile16 + 2 * s * 128, 128, kSbo16);
+                mma3(d, re_h, re_l, c_h, c_l, id32, s ? 1u : 0u);
+                mma3(d, im_h, im_l, s_h, s_l, id32n, 1u);
               }
-              tc::commit(&bar);
+              tc::commit(&bar_t[st & 1]);
             }
-            mma_done();
-            // ---- D3 -> output rows (y, z), 32 t each
-            {
+          }
+          if (prev_y >= 0) {
+            // ---- store D3 of the previous step: rows (y % 8, zl) -> (y, z), 32 t
+            if ((st - 1) & 1) {
+              tc::mbar_wait(&bar_t[1], ph_t1);
+              ph_t1 ^= 1;
+            } else {
+              tc::mbar_wait(&bar_t[0], ph_t0);
+              ph_t0 ^= 1;
+            }
+            tc::fence_after();
+            if (part == 0) {
               float v[32];
-              const int tile = part;
-              tc::tmem_ld32(d3 + ((uint32_t)(32 * quarter) << 16) + 32 * tile, v);
+              tc::tmem_ld32(d3 + 32 * ((st - 1) & 1) + ((uint32_t)(32 * quarter) << 16), v);
               const int m = 32 * quarter + lane;
-              const int y = yc * 16 + tile * 8 + (m >> 4), z = zc * 64 + zb * 16 + (m & 15);
-              const int t0 = tb * kTileT;
+              const int y = prev_y + (m >> 4), z = prev_z + (m & 15);
               if (y < Ny && z < Nz) {
-                float* row = o_slab + (long long)y * plane + (long long)z * Nt + t0;
-                if (vec_out && t0 + kTileT <= Nt) {
+                float* row = o_slab + (long long)y * plane + (long long)z * Nt + prev_t0;
+                if (vec_out && prev_t0 + kTileT <= Nt) {
 #pragma unroll
                   for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<float4*>(row + 4 * q) =
-                        make_float4(scale * v[4 * q], scale * v[4 * q + 1], scale * v[4 * q + 2], scale * v[4 * q + 3]);
+                    __stcs(reinterpret_cast<float4*>(row + 4 * q),
+                           make_float4(scale * v[4 * q], scale * v[4 * q + 1], scale * v[4 * q + 2],
+                                       scale * v[4 * q + 3]));
                 } else {
 #pragma unroll
                   for (int t = 0; t < 32; ++t)
-                    if (t0 + t < Nt) row[t] = scale * v[t];
+                    if (prev_t0 + t < Nt) row[t] = scale * v[t];
                 }
               }
             }
-            tc::fence_before();
-            __syncthreads();
+          }
+          if (st < n_steps) {
+            const int tb = st % n_tb, tile = (st / n_tb) & 1, zb = st / (2 * n_tb);
+            prev_y = yc * 16 + tile * 8;
+            prev_z = zc * 64 + zb * 16;
+            prev_t0 = tb * kTileT;
           }
         }
+        tc::fence_before();
+        __syncthreads();
       }
     }
   }
@@ -719,34 +774,21 @@ static bool supported(const dfno_geom& g) {
 
 static constexpr int kSmemCap = 225 * 1024;
 
-template <int MODE, bool VEC, int STAGES>
-static int launch_fwd_s(const dfno_geom& g, const void* src, const void* pre, double scale, void* out,
-                        cudaStream_t st) {
-  const FwdLayout L = fwd_layout(g.ny, g.nz, g.nt, STAGES, MODE == DFNO_SRC_GRAD);
-  const size_t smem = (size_t)L.total;
-  auto kern = k_yzt_fwd_tc<MODE, VEC, STAGES>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return DFNO_ERR_UNSUPPORTED;
-  const int slabs = g.batch * g.c * x_local(g);
-  const int grid = sm_count() < slabs ? sm_count() : slabs;
-  kern<<<grid, kThreads, smem, st>>>(g, (const float*)src, (const float*)pre, (float)scale, (float2*)out);
-  DFNO_CUDA_CHECK_LAUNCH();
-  return DFNO_OK;
-}
-
 template <int MODE, bool VEC>
 static int launch_fwd(const dfno_geom& g, const void* src, const void* pre, double scale, void* out,
                       cudaStream_t st) {
-  const bool grad = MODE == DFNO_SRC_GRAD;
-  if (fwd_layout(g.ny, g.nz, g.nt, 5, grad).total <= kSmemCap)
-    return launch_fwd_s<MODE, VEC, 5>(g, src, pre, scale, out, st);
-  if (fwd_layout(g.ny, g.nz, g.nt, 4, grad).total <= kSmemCap)
-    return launch_fwd_s<MODE, VEC, 4>(g, src, pre, scale, out, st);
-  if (fwd_layout(g.ny, g.nz, g.nt, 3, grad).total <= kSmemCap)
-    return launch_fwd_s<MODE, VEC, 3>(g, src, pre, scale, out, st);
-  if (fwd_layout(g.ny, g.nz, g.nt, 2, grad).total <= kSmemCap)
-    return launch_fwd_s<MODE, VEC, 2>(g, src, pre, scale, out, st);
-  return DFNO_ERR_UNSUPPORTED;
+  // tiles held in registers ahead of use: 3 (one input) / 2 (grad: two inputs)
+  constexpr int PF = (MODE == DFNO_SRC_GRAD) ? 2 : 3;
+  const FwdLayout L = fwd_layout(g.ny, g.nz, g.nt);
+  if (L.total > kSmemCap) return DFNO_ERR_UNSUPPORTED;
+  auto kern = k_yzt_fwd_tc<MODE, VEC, PF>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  const int slabs = g.batch * g.c * x_local(g);
+  const int grid = sm_count() < slabs ? sm_count() : slabs;
+  kern<<<grid, kThreads, L.total, st>>>(g, (const float*)src, (const float*)pre, (float)scale, (float2*)out);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
 }
 
 int yzt_fwd_tc(const dfno_geom& g, const void* src, const void* pre, int mode, double scale, void* out,

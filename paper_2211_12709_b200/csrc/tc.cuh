@@ -115,14 +115,27 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok;
+}
+
+// Wait for the phase with the given parity to complete.  Watchdog: a wait
+// longer than ~2^35 cycles (tens of seconds) traps, turning a pipeline
+// deadlock into a launch error instead of a hung GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 35)) __trap();
+  }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -153,6 +166,12 @@ __device__ __forceinline__ float round_tf32(float x) {
 __device__ __forceinline__ void split_rn(float x, float& hi, float& lo) {
   hi = round_tf32(x);
   lo = round_tf32(x - hi);
+}
+// Cheaper split for streamed data: hi rounded, lo left for the tensor core's
+// truncation (|lo| <= 2^-11 |x|, so its truncation error is <= 2^-21 |x|).
+__device__ __forceinline__ void split_hl(float x, float& hi, float& lo) {
+  hi = round_tf32(x);
+  lo = x - hi;
 }
 
 // ---- cp.async (LDGSTS): 16-byte and 4-byte copies with zero fill ---------
