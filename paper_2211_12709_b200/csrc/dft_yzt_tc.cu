@@ -41,13 +41,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTileT = 32;                         // t per stage-T K block
-constexpr int kRawBytes = 128 * kTileT * 4;        // one raw staged tile (16 KB)
 // forward operand tiles (bytes)
 constexpr int kLboT = 144, kSboT = 1152, kATBytes = 16 * kSboT;
 constexpr int kLboZ = 160, kSboZ = 608, kAZBytes = 16 * kSboZ;
 constexpr int kLboY = 192, kSboY = 320, kTileYBytes = 16 * kSboY;
 constexpr int kAYBytes = 8 * kTileYBytes;          // (re, im) x (hi, lo) x 2 tiles
-constexpr int kATRegion = (2 * kATBytes > kAYBytes) ? 2 * kATBytes : kAYBytes;  // A_T aliases A_Y
 // inverse operand tiles: 128 rows x K = 16, LBO 128, SBO 528
 constexpr int kSbo16 = 528, kTile16 = 16 * kSbo16;
 constexpr int kBSbo16 = 512;                       // twiddle B with K = 16
@@ -79,8 +77,8 @@ __device__ __forceinline__ void sincos_idx(long long k, int n, int N, double& s,
 
 template <int MODE>
 __device__ __forceinline__ float transform(float v, float p, int act) {
-  if (MODE == DFNO_SRC_ACT) return act == DFNO_ACT_GELU ? tc::gelu_fast(v) : act_apply<float>(act, v);
-  if (MODE == DFNO_SRC_GRAD) return v * (act == DFNO_ACT_GELU ? tc::gelu_grad_fast(p) : act_deriv<float>(act, p));
+  if (MODE == DFNO_SRC_ACT) return act_apply<float>(act, v);
+  if (MODE == DFNO_SRC_GRAD) return v * act_deriv<float>(act, p);
   return v;
 }
 
@@ -127,7 +125,7 @@ __host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt) {
   L.sbo_bz = (L.NZ16 / 4) * 128;
   L.sbo_by = (L.NY8 / 4) * 128;
   int o = 0;
-  L.off_at = o; o += 2 * kATBytes;
+  L.off_at = o; o += 4 * kATBytes;  // 2 buffers x (hi, lo)
   L.off_az = o; o += 4 * kAZBytes;
   L.off_ay = o; o += kAYBytes;
   L.off_bt = o; o += 2 * 4 * L.sbo_bt;
@@ -137,49 +135,67 @@ __host__ __device__ inline FwdLayout fwd_layout(int ny, int nz, int nt) {
   return L;
 }
 
-// Walks the tiles (slab, y chunk, z block, t block) of one CTA in order
-// without divisions in the steady state.
+// Walks the tiles (slab, y chunk, z block, t block) of one CTA in order.
 struct TileCursor {
   int slab, yc, zb, tb;
-  long long base;  // element offset of the slab
-  __device__ void set_slab(const dfno_geom& g, int s, int XL, long long slab_elems) {
+  long long base;  // element offset of the slab ((b, c, x) slabs are contiguous)
+  __device__ void start(int s, long long slab_elems) {
     slab = s;
-    base = (long long)s * slab_elems;  // slabs are contiguous (b, c, x) in the activation layout
-    (void)g;
-    (void)XL;
+    yc = zb = tb = 0;
+    base = (long long)s * slab_elems;
   }
-  __device__ void advance(const dfno_geom& g, int n_yc, int n_zb, int n_tb, int XL, long long slab_elems) {
+  __device__ void advance(int n_yc, int n_zb, int n_tb, long long slab_elems) {
     if (++tb < n_tb) return;
     tb = 0;
     if (++zb < n_zb) return;
     zb = 0;
     if (++yc < n_yc) return;
-    yc = 0;
-    set_slab(g, slab + (int)gridDim.x, XL, slab_elems);
+    start(slab + (int)gridDim.x, slab_elems);
   }
 };
+
+// (slab, y chunk, z block) group walk
+struct GroupCursor {
+  int slab, yc, zb;
+  __device__ void advance(int n_yc, int n_zb) {
+    if (++zb < n_zb) return;
+    zb = 0;
+    if (++yc < n_yc) return;
+    yc = 0;
+    slab += (int)gridDim.x;
+  }
+};
+
+constexpr int kConvWarps = 8, kEpiWarps = 4;
+constexpr int kFwdThreads = (kConvWarps + kEpiWarps + 1) * 32;  // + 1 MMA warp
 
 }  // namespace
 
 // ===========================================================================
-// forward
+// forward: warp-specialised
+//   warps 0-7  converters : global -> registers (PF tiles ahead) -> act /
+//                           grad*act' -> 3xTF32 split -> A_T[2] ring
+//   warps 8-11 epilogue   : D1 (TMEM) -> A_Z ; D2 -> A_Y ; D3 -> XK output
+//   warp 12    MMA issuer : stage T / Z / Y tcgen05.mma, commits to mbarriers
+// Every hand-off is an mbarrier full / empty pair; no block-wide barrier in
+// the steady state.
 // ===========================================================================
 template <int MODE, bool VEC, int PF>
-__global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, const float* __restrict__ src,
-                                                            const float* __restrict__ pre, float scale,
-                                                            float2* __restrict__ out) {
+__global__ void __launch_bounds__(kFwdThreads, 1) k_yzt_fwd_tc(const dfno_geom g, const float* __restrict__ src,
+                                                               const float* __restrict__ pre, float scale,
+                                                               float2* __restrict__ out) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
-  constexpr int NV = VEC ? 4 : 16;  // loads per thread per tile (float4 or float)
+  constexpr int NV = VEC ? 4 : 16;  // loads per converter thread per tile
   using LT = typename std::conditional<VEC, float4, float>::type;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar_t, bar_z, bar_y;
+  __shared__ uint64_t at_full[2], at_empty[2], d1_full[2], d1_empty[2];
+  __shared__ uint64_t az_full, az_empty, d2_full, d2_empty, ay_full, ay_empty, d3_full, d3_empty;
   __shared__ uint32_t tmem_base;
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
   const FwdLayout L = fwd_layout(Ny, Nz, Nt);
-  unsigned char* at_hi = smem + L.off_at;
-  unsigned char* at_lo = at_hi + kATBytes;
+  unsigned char* at = smem + L.off_at;
   unsigned char* az = smem + L.off_az;
   unsigned char* ay = smem + L.off_ay;
   unsigned char* bt = smem + L.off_bt;
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
   // ---- twiddles ---------------------------------------------------------
   {
     const int plane = 4 * L.sbo_bt;  // 32 rows
-    for (int e = tid; e < 32 * L.KT; e += kThreads) {
+    for (int e = tid; e < 32 * L.KT; e += blockDim.x) {
       const int n = e / L.KT, t = e % L.KT, kt = n & 15;
       double c = 0.0, s = 0.0;
       if (kt < g.rt && t < Nt) sincos_idx(mode_freq(kt, Nt, g.mt), t, Nt, s, c);
@@ -209,9 +225,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
   });
   if (warp == 0) tc::tmem_alloc<kFwdTmemCols>(&tmem_base);
   if (tid == 0) {
-    tc::mbar_init(&bar_t, 1);
-    tc::mbar_init(&bar_z, 1);
-    tc::mbar_init(&bar_y, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&at_full[b], kConvWarps * 32);
+      tc::mbar_init(&at_empty[b], 1);
+      tc::mbar_init(&d1_full[b], 1);
+      tc::mbar_init(&d1_empty[b], kEpiWarps * 32);
+    }
+    tc::mbar_init(&az_full, kEpiWarps * 32);
+    tc::mbar_init(&az_empty, 1);
+    tc::mbar_init(&d2_full, 1);
+    tc::mbar_init(&d2_empty, kEpiWarps * 32);
+    tc::mbar_init(&ay_full, kEpiWarps * 32);
+    tc::mbar_init(&ay_empty, 1);
+    tc::mbar_init(&d3_full, 1);
+    tc::mbar_init(&d3_empty, kEpiWarps * 32);
     tc::mbar_fence_init();
   }
   tc::fence_proxy_async();
@@ -224,264 +251,272 @@ __global__ void __launch_bounds__(kThreads, 1) k_yzt_fwd_tc(const dfno_geom g, c
   const int n_yc = (Ny + 7) / 8, n_zb = (Nz + 15) / 16, n_tb = L.KT / kTileT;
   const int slabs = g.batch * g.c * XL;
   const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int total = my_slabs * n_yc * n_zb * n_tb;
+  const int n_groups = my_slabs * n_yc * n_zb;
+  const int n_tiles = n_groups * n_tb;
   const long long plane = (long long)Nz * Nt;
   const long long slab_elems = (long long)Ny * plane;
-  const int quarter = warp & 3, part = warp >> 2;
 
-  const uint32_t id_t = tc::idesc_tf32(128, 32);
-  const uint32_t id16 = tc::idesc_tf32(128, 16);
-  const uint32_t id16n = tc::idesc_tf32(128, 16, false, true);
-  const uint32_t s_at_hi = tc::smem_u32(at_hi), s_at_lo = tc::smem_u32(at_lo);
-  const uint32_t s_az = tc::smem_u32(az), s_ay = tc::smem_u32(ay);
-  const uint32_t s_bt = tc::smem_u32(bt), s_bz = tc::smem_u32(bz), s_by = tc::smem_u32(by);
-
-  // per-thread tile geometry (tile rows = (y, z) = 8 x 16, 32 t):
-  //   VEC    : row = (tid >> 3) + 32 j -> y = (tid >> 7) + 2 j, z = (tid >> 3) & 15, t = 4 (tid & 7)
-  //   scalar : row = (tid >> 5) + 8 j  -> y = j >> 1, z = (tid >> 5) + 8 (j & 1),    t = tid & 31
-  const int tt = VEC ? 4 * (tid & 7) : (tid & 31);
-
-  LT buf[PF][NV];
-  LT pbuf[GRAD ? PF : 1][GRAD ? NV : 1];
-
-  auto load_tile = [&](const TileCursor& c, LT (&b)[NV], LT (&pb)[GRAD ? NV : 1]) {
-    const int y0 = c.yc * 8, z0 = c.zb * 16, t = c.tb * kTileT + tt;
-    const bool t_ok = t < Nt;
+  if (warp < kConvWarps) {
+    // ======================= converters =======================
+    const int ct = tid;  // 0 .. 255
+    const int tt = VEC ? 4 * (ct & 7) : (ct & 31);
+    LT buf[PF][NV];
+    LT pbuf[GRAD ? PF : 1][GRAD ? NV : 1];
+    auto load_tile = [&](const TileCursor& c, LT (&b)[NV], LT (&pb)[GRAD ? NV : 1]) {
+      const int y0 = c.yc * 8, z0 = c.zb * 16, t = c.tb * kTileT + tt;
+      const bool t_ok = t < Nt;
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int y = VEC ? y0 + (tid >> 7) + 2 * j : y0 + (j >> 1);
-      const int z = VEC ? z0 + ((tid >> 3) & 15) : z0 + (tid >> 5) + 8 * (j & 1);
-      const bool ok = t_ok && (z < Nz) && (y < Ny);
-      const long long off = c.base + (long long)y * plane + (long long)z * Nt + t;
-      if constexpr (VEC) {
-        b[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if constexpr (GRAD)
-          pb[j] = ok ? __ldg(reinterpret_cast<const float4*>(pre + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        b[j] = ok ? __ldg(src + off) : 0.f;
-        if constexpr (GRAD) pb[j] = ok ? __ldg(pre + off) : 0.f;
+      for (int j = 0; j < NV; ++j) {
+        // VEC:    row = (ct >> 3) + 32 j -> y = (ct >> 7) + 2 j, z = (ct >> 3) & 15
+        // scalar: row = (ct >> 5) + 8 j  -> y = j >> 1,          z = (ct >> 5) + 8 (j & 1)
+        const int y = VEC ? y0 + (ct >> 7) + 2 * j : y0 + (j >> 1);
+        const int z = VEC ? z0 + ((ct >> 3) & 15) : z0 + (ct >> 5) + 8 * (j & 1);
+        const bool ok = t_ok && (z < Nz) && (y < Ny);
+        const long long off = c.base + (long long)y * plane + (long long)z * Nt + t;
+        if constexpr (VEC) {
+          b[j] = ok ? __ldg(reinterpret_cast<const float4*>(src + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (GRAD)
+            pb[j] = ok ? __ldg(reinterpret_cast<const float4*>(pre + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          b[j] = ok ? __ldg(src + off) : 0.f;
+          if constexpr (GRAD) pb[j] = ok ? __ldg(pre + off) : 0.f;
+        }
       }
-    }
-  };
-  auto convert_tile = [&](LT (&b)[NV], LT (&pb)[GRAD ? NV : 1]) {
+    };
+    auto convert_tile = [&](LT (&b)[NV], LT (&pb)[GRAD ? NV : 1], unsigned char* hi, unsigned char* lo) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      if constexpr (VEC) {
-        float4 v = b[j];
-        float4 p = GRAD ? pb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
-        v.x = transform<MODE>(v.x, p.x, g.act);
-        v.y = transform<MODE>(v.y, p.y, g.act);
-        v.z = transform<MODE>(v.z, p.z, g.act);
-        v.w = transform<MODE>(v.w, p.w, g.act);
-        float4 h, l;
-        tc::split_hl(v.x, h.x, l.x);
-        tc::split_hl(v.y, h.y, l.y);
-        tc::split_hl(v.z, h.z, l.z);
-        tc::split_hl(v.w, h.w, l.w);
-        const int row = (tid >> 3) + 32 * j;
-        const int off = (row >> 3) * kSboT + (tid & 7) * kLboT + (row & 7) * 16;
-        *reinterpret_cast<float4*>(at_hi + off) = h;
-        *reinterpret_cast<float4*>(at_lo + off) = l;
-      } else {
-        const float v = transform<MODE>(b[j], GRAD ? pb[j] : 0.f, g.act);
-        const int row = (tid >> 5) + 8 * j;
-        float h, l;
-        tc::split_hl(v, h, l);
-        const int off = kmaj(row, tid & 31, kLboT, kSboT);
-        *reinterpret_cast<float*>(at_hi + off) = h;
-        *reinterpret_cast<float*>(at_lo + off) = l;
+      for (int j = 0; j < NV; ++j) {
+        if constexpr (VEC) {
+          float4 v = b[j];
+          const float4 p = GRAD ? pb[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+          v.x = transform<MODE>(v.x, p.x, g.act);
+          v.y = transform<MODE>(v.y, p.y, g.act);
+          v.z = transform<MODE>(v.z, p.z, g.act);
+          v.w = transform<MODE>(v.w, p.w, g.act);
+          float4 h, l;
+          tc::split_hl(v.x, h.x, l.x);
+          tc::split_hl(v.y, h.y, l.y);
+          tc::split_hl(v.z, h.z, l.z);
+          tc::split_hl(v.w, h.w, l.w);
+          const int row = (ct >> 3) + 32 * j;
+          const int off = (row >> 3) * kSboT + (ct & 7) * kLboT + (row & 7) * 16;
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = l;
+        } else {
+          const float v = transform<MODE>(b[j], GRAD ? pb[j] : 0.f, g.act);
+          const int row = (ct >> 5) + 8 * j;
+          float h, l;
+          tc::split_hl(v, h, l);
+          const int off = kmaj(row, ct & 31, kLboT, kSboT);
+          *reinterpret_cast<float*>(hi + off) = h;
+          *reinterpret_cast<float*>(lo + off) = l;
+        }
       }
-    }
-  };
-
-  TileCursor lc, pc;
-  lc.yc = lc.zb = lc.tb = 0;
-  lc.set_slab(g, blockIdx.x, XL, slab_elems);
-  pc = lc;
-#pragma unroll
-  for (int k = 0; k < PF; ++k) {
-    if (k < total) {
-      if constexpr (GRAD) load_tile(lc, buf[k], pbuf[k]);
-      else load_tile(lc, buf[k], pbuf[0]);
-      lc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
-    }
-  }
-
-  uint32_t ph_t = 0, ph_z = 0, ph_y = 0;
-  bool z_pending = false, y_pending = false;
-  int group = 0;  // (y chunk, z block) group counter -> D1 buffer parity
-  TileCursor ec;  // cursor of the group awaiting its epilogue
-  bool ep_pending = false;
-
-  // epilogue of a finished (yc, zb) group: D1 -> A_Z -> stage Z (+ chunk / slab ends)
-  auto epilogue = [&](const TileCursor& c, int grp) {
-    if (z_pending) {
-      tc::mbar_wait(&bar_z, ph_z);
-      ph_z ^= 1;
-      z_pending = false;
-    }
-    tc::fence_after();
-    {
-      float v[16];
-      tc::tmem_ld16(tmem + 32 * (grp & 1) + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
-      const int r = 32 * quarter + lane, y = r >> 4, zl = r & 15;  // D1 row = (y, zl)
-      unsigned char* hi = az + part * 2 * kAZBytes;
-      unsigned char* lo = hi + kAZBytes;
-      const int base = (zl >> 2) * kLboZ + y * 16 + (zl & 3) * 4;  // A_Z row = (kt, y), k = zl
-#pragma unroll
-      for (int kt = 0; kt < 16; ++kt) st_split(hi, lo, kt * kSboZ + base, v[kt]);
-    }
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint32_t pl = 2 * L.sbo_bz;
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const uint32_t ka = 2 * s * kLboZ, kb = (uint32_t)(c.zb * 4 + 2 * s) * 128;
-        const uint64_t re_h = tc::desc(s_az + 0 * kAZBytes + ka, kLboZ, kSboZ);
-        const uint64_t re_l = tc::desc(s_az + 1 * kAZBytes + ka, kLboZ, kSboZ);
-        const uint64_t im_h = tc::desc(s_az + 2 * kAZBytes + ka, kLboZ, kSboZ);
-        const uint64_t im_l = tc::desc(s_az + 3 * kAZBytes + ka, kLboZ, kSboZ);
-        const uint64_t c_h = tc::desc(s_bz + 0 * pl + kb, 128, L.sbo_bz);
-        const uint64_t c_l = tc::desc(s_bz + 1 * pl + kb, 128, L.sbo_bz);
-        const uint64_t s_h = tc::desc(s_bz + 2 * pl + kb, 128, L.sbo_bz);
-        const uint64_t s_l = tc::desc(s_bz + 3 * pl + kb, 128, L.sbo_bz);
-        const uint32_t first = (c.zb == 0 && s == 0) ? 0u : 1u;
-        // e^{-i}: re += A_re C + A_im S ;  im += A_im C - A_re S
-        mma3(d2, re_h, re_l, c_h, c_l, id16, first);
-        mma3(d2, im_h, im_l, s_h, s_l, id16, 1u);
-        mma3(d2 + 16, im_h, im_l, c_h, c_l, id16, first);
-        mma3(d2 + 16, re_h, re_l, s_h, s_l, id16n, 1u);
-      }
-      tc::commit(&bar_z);
-    }
-    z_pending = true;
-    if (c.zb != n_zb - 1) return;
-    // ---- chunk end: D2 -> A_Y -> stage Y
-    tc::mbar_wait(&bar_z, ph_z);
-    ph_z ^= 1;
-    z_pending = false;
-    if (y_pending) {
-      tc::mbar_wait(&bar_y, ph_y);
-      ph_y ^= 1;
-      y_pending = false;
-    }
-    tc::fence_after();
-    {
-      float v[16];
-      tc::tmem_ld16(d2 + ((uint32_t)(32 * quarter) << 16) + 16 * part, v);
-      const int m = 32 * quarter + lane, kt = m >> 3, y = m & 7;  // D2 row = (kt, y)
-      unsigned char* hi = ay + part * 4 * kTileYBytes;
-      unsigned char* lo = hi + 2 * kTileYBytes;
-      const int base = (kt >> 3) * kSboY + (y >> 2) * kLboY + (kt & 7) * 16 + (y & 3) * 4;
-#pragma unroll
-      for (int kz = 0; kz < 16; ++kz)  // A_Y row = (kz % 8, kt) in tile kz / 8, k = y
-        st_split(hi, lo, (kz >> 3) * kTileYBytes + (kz & 7) * 2 * kSboY + base, v[kz]);
-    }
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint32_t kb = (uint32_t)(c.yc * 2) * 128, pl = 2 * L.sbo_by;
-      const uint64_t c_h = tc::desc(s_by + 0 * pl + kb, 128, L.sbo_by);
-      const uint64_t c_l = tc::desc(s_by + 1 * pl + kb, 128, L.sbo_by);
-      const uint64_t s_h = tc::desc(s_by + 2 * pl + kb, 128, L.sbo_by);
-      const uint64_t s_l = tc::desc(s_by + 3 * pl + kb, 128, L.sbo_by);
-      const uint32_t first = (c.yc == 0) ? 0u : 1u;
-#pragma unroll
-      for (int tile = 0; tile < 2; ++tile) {
-        const uint32_t a0 = s_ay + tile * kTileYBytes;
-        const uint64_t re_h = tc::desc(a0 + 0 * kTileYBytes, kLboY, kSboY);
-        const uint64_t re_l = tc::desc(a0 + 2 * kTileYBytes, kLboY, kSboY);
-        const uint64_t im_h = tc::desc(a0 + 4 * kTileYBytes, kLboY, kSboY);
-        const uint64_t im_l = tc::desc(a0 + 6 * kTileYBytes, kLboY, kSboY);
-        const uint32_t dre = d3 + 32 * tile, dim = dre + 16;
-        mma3(dre, re_h, re_l, c_h, c_l, id16, first);
-        mma3(dre, im_h, im_l, s_h, s_l, id16, 1u);
-        mma3(dim, im_h, im_l, c_h, c_l, id16, first);
-        mma3(dim, re_h, re_l, s_h, s_l, id16n, 1u);
-      }
-      tc::commit(&bar_y);
-    }
-    y_pending = true;
-    if (c.yc != n_yc - 1) return;
-    // ---- slab end: D3 -> XK exchange layout
-    tc::mbar_wait(&bar_y, ph_y);
-    ph_y ^= 1;
-    y_pending = false;
-    tc::fence_after();
-    {
-      const int slab = c.slab, xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
-      float v[32];
-      tc::tmem_ld32(d3 + ((uint32_t)(32 * quarter) << 16) + 32 * part, v);
-      const int m = 32 * quarter + lane, kz = 8 * part + (m >> 4), kt = m & 15;
-      if (kz < g.rz && kt < g.rt) {
-#pragma unroll
-        for (int ky = 0; ky < 16; ++ky)
-          if (ky < g.ry)
-            out[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt] = make_float2(scale * v[ky], scale * v[16 + ky]);
-      }
-    }
-    tc::fence_before();
-    __syncthreads();
-  };
-
-  // one tile: convert (prefetched registers) -> A_T, refill the registers,
-  // stage-T MMAs, then the lagging epilogue of the previous group
-  auto step = [&](LT (&b)[NV], LT (&pb)[GRAD ? NV : 1], int i) {
-    if (i > 0) {  // A_T free: stage T of the previous tile finished
-      tc::mbar_wait(&bar_t, ph_t);
-      ph_t ^= 1;
-    }
-    convert_tile(b, pb);
-    if (i + PF < total) {
-      load_tile(lc, b, pb);
-      lc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
-    }
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint32_t dd = tmem + 32 * (group & 1);
-#pragma unroll
-      for (int s = 0; s < kTileT / 8; ++s) {
-        const uint32_t ka = 2 * s * kLboT, kb = (uint32_t)(pc.tb * (kTileT / 4) + 2 * s) * 128;
-        mma3(dd, tc::desc(s_at_hi + ka, kLboT, kSboT), tc::desc(s_at_lo + ka, kLboT, kSboT),
-             tc::desc(s_bt + kb, 128, L.sbo_bt), tc::desc(s_bt + 4 * L.sbo_bt + kb, 128, L.sbo_bt), id_t,
-             (pc.tb > 0 || s > 0) ? 1u : 0u);
-      }
-      tc::commit(&bar_t);
-    }
-    if (ep_pending) {
-      epilogue(ec, group - 1);
-      ep_pending = false;
-    }
-    if (pc.tb == n_tb - 1) {  // this group is complete once its last stage-T lands
-      ec = pc;
-      ep_pending = true;
-      ++group;
-    }
-    pc.advance(g, n_yc, n_zb, n_tb, XL, slab_elems);
-  };
-
-#pragma unroll 1
-  for (int i0 = 0; i0 < total; i0 += PF) {
+    };
+    TileCursor lc;
+    lc.start(blockIdx.x, slab_elems);
 #pragma unroll
     for (int k = 0; k < PF; ++k) {
-      if (i0 + k < total) {
-        if constexpr (GRAD) step(buf[k], pbuf[k], i0 + k);
-        else step(buf[k], pbuf[0], i0 + k);
+      if (k < n_tiles) {
+        if constexpr (GRAD) load_tile(lc, buf[k], pbuf[k]);
+        else load_tile(lc, buf[k], pbuf[0]);
+        lc.advance(n_yc, n_zb, n_tb, slab_elems);
       }
     }
-  }
-  if (total > 0) {
-    tc::mbar_wait(&bar_t, ph_t);
-    ph_t ^= 1;
-    if (ep_pending) epilogue(ec, group - 1);
+#pragma unroll 1
+    for (int i0 = 0; i0 < n_tiles; i0 += PF) {
+#pragma unroll
+      for (int k = 0; k < PF; ++k) {
+        const int i = i0 + k;
+        if (i < n_tiles) {
+          const int ab = i & 1;
+          tc::mbar_wait(&at_empty[ab], ((i >> 1) & 1) ^ 1);
+          unsigned char* hi = at + ab * 2 * kATBytes;
+          if constexpr (GRAD) convert_tile(buf[k], pbuf[k], hi, hi + kATBytes);
+          else convert_tile(buf[k], pbuf[0], hi, hi + kATBytes);
+          if (i + PF < n_tiles) {
+            if constexpr (GRAD) load_tile(lc, buf[k], pbuf[k]);
+            else load_tile(lc, buf[k], pbuf[0]);
+            lc.advance(n_yc, n_zb, n_tb, slab_elems);
+          }
+          tc::fence_proxy_async();
+          tc::mbar_arrive(&at_full[ab]);
+        }
+      }
+    }
+  } else if (warp < kConvWarps + kEpiWarps) {
+    // ======================= epilogue =======================
+    const int quarter = warp & 3;
+    const int m = 32 * quarter + lane;  // TMEM lane / operand row
+    const uint32_t lane_off = (uint32_t)(32 * quarter) << 16;
+    GroupCursor gc{(int)blockIdx.x, 0, 0};
+    int chunk = 0, slab_i = 0;
+#pragma unroll 1
+    for (int G = 0; G < n_groups; ++G) {
+      const int d1b = G & 1;
+      tc::mbar_wait(&d1_full[d1b], (G >> 1) & 1);
+      tc::fence_after();
+      float v[32];
+      tc::tmem_ld32(tmem + 32 * d1b + lane_off, v);  // row (y, zl): re[kt] 0..15, im[kt] 16..31
+      tc::fence_before();
+      tc::mbar_arrive(&d1_empty[d1b]);
+      tc::mbar_wait(&az_empty, (G & 1) ^ 1);
+      {
+        const int y = m >> 4, zl = m & 15;
+        const int base = (zl >> 2) * kLboZ + y * 16 + (zl & 3) * 4;  // A_Z row = (kt, y), k = zl
+#pragma unroll
+        for (int kt = 0; kt < 16; ++kt) {
+          st_split(az + 0 * kAZBytes, az + 1 * kAZBytes, kt * kSboZ + base, v[kt]);
+          st_split(az + 2 * kAZBytes, az + 3 * kAZBytes, kt * kSboZ + base, v[16 + kt]);
+        }
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&az_full);
+      if (gc.zb == n_zb - 1) {
+        // ---- chunk end: D2 -> A_Y
+        tc::mbar_wait(&d2_full, chunk & 1);
+        tc::fence_after();
+        tc::tmem_ld32(d2 + lane_off, v);  // row (kt, y): re[kz] 0..15, im[kz] 16..31
+        tc::fence_before();
+        tc::mbar_arrive(&d2_empty);
+        tc::mbar_wait(&ay_empty, (chunk & 1) ^ 1);
+        {
+          const int kt = m >> 3, y = m & 7;
+          const int base = (kt >> 3) * kSboY + (y >> 2) * kLboY + (kt & 7) * 16 + (y & 3) * 4;
+#pragma unroll
+          for (int kz = 0; kz < 16; ++kz) {  // A_Y row = (kz % 8, kt) of tile kz / 8, k = y
+            const int off = (kz >> 3) * kTileYBytes + (kz & 7) * 2 * kSboY + base;
+            st_split(ay + 0 * kTileYBytes, ay + 2 * kTileYBytes, off, v[kz]);
+            st_split(ay + 4 * kTileYBytes, ay + 6 * kTileYBytes, off, v[16 + kz]);
+          }
+        }
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&ay_full);
+        ++chunk;
+        if (gc.yc == n_yc - 1) {
+          // ---- slab end: D3 -> XK exchange layout
+          tc::mbar_wait(&d3_full, slab_i & 1);
+          tc::fence_after();
+          const int slab = gc.slab, xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+#pragma unroll
+          for (int tile = 0; tile < 2; ++tile) {
+            tc::tmem_ld32(d3 + 32 * tile + lane_off, v);
+            const int kz = 8 * tile + (m >> 4), kt = m & 15;
+            if (kz < g.rz && kt < g.rt) {
+#pragma unroll
+              for (int ky = 0; ky < 16; ++ky)
+                if (ky < g.ry)
+                  out[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt] = make_float2(scale * v[ky], scale * v[16 + ky]);
+            }
+          }
+          tc::fence_before();
+          tc::mbar_arrive(&d3_empty);
+          ++slab_i;
+        }
+      }
+      gc.advance(n_yc, n_zb);
+    }
+  } else if (lane == 0) {
+    // ======================= MMA issuer =======================
+    const uint32_t id_t = tc::idesc_tf32(128, 32);
+    const uint32_t id16 = tc::idesc_tf32(128, 16);
+    const uint32_t id16n = tc::idesc_tf32(128, 16, false, true);
+    const uint32_t s_at = tc::smem_u32(at), s_az = tc::smem_u32(az), s_ay = tc::smem_u32(ay);
+    const uint32_t s_bt = tc::smem_u32(bt), s_bz = tc::smem_u32(bz), s_by = tc::smem_u32(by);
+    GroupCursor gT{(int)blockIdx.x, 0, 0}, gZ = gT, gY = gT;  // groups for the T, Z and Y jobs
+    int tile = 0, zchunk = 0, yslab = 0, ygroup = 0;
+#pragma unroll 1
+    for (int G = 0; G < n_groups + 2; ++G) {
+      if (G < n_groups) {
+        // ---- stage T for all t blocks of group G -> D1[G & 1]
+        const int d1b = G & 1;
+        tc::mbar_wait(&d1_empty[d1b], ((G >> 1) & 1) ^ 1);
+        for (int tb = 0; tb < n_tb; ++tb, ++tile) {
+          const int ab = tile & 1;
+          tc::mbar_wait(&at_full[ab], (tile >> 1) & 1);
+          tc::fence_after();
+          const uint32_t a0 = s_at + ab * 2 * kATBytes;
+#pragma unroll
+          for (int s = 0; s < kTileT / 8; ++s) {
+            const uint32_t ka = 2 * s * kLboT, kb = (uint32_t)(tb * (kTileT / 4) + 2 * s) * 128;
+            mma3(tmem + 32 * d1b, tc::desc(a0 + ka, kLboT, kSboT), tc::desc(a0 + kATBytes + ka, kLboT, kSboT),
+                 tc::desc(s_bt + kb, 128, L.sbo_bt), tc::desc(s_bt + 4 * L.sbo_bt + kb, 128, L.sbo_bt), id_t,
+                 (tb > 0 || s > 0) ? 1u : 0u);
+          }
+          tc::commit(&at_empty[ab]);
+        }
+        tc::commit(&d1_full[d1b]);
+        gT.advance(n_yc, n_zb);
+      }
+      // order: Y(G-2) before Z(G-1) -- the epilogue's slab end waits for
+      // Y(G-2) before it can hand over A_Z of group G-1
+      if (G >= 2 && G - 2 < n_groups) {
+        const bool chunk_end = (gY.zb == n_zb - 1);
+        if (chunk_end) {
+          // ---- stage Y for the chunk that group G - 2 completed -> D3
+          tc::mbar_wait(&ay_full, ygroup & 1);
+          if (gY.yc == 0) tc::mbar_wait(&d3_empty, (yslab & 1) ^ 1);
+          tc::fence_after();
+          const uint32_t kb = (uint32_t)(gY.yc * 2) * 128, pl = 2 * L.sbo_by;
+          const uint64_t c_h = tc::desc(s_by + 0 * pl + kb, 128, L.sbo_by);
+          const uint64_t c_l = tc::desc(s_by + 1 * pl + kb, 128, L.sbo_by);
+          const uint64_t s_h = tc::desc(s_by + 2 * pl + kb, 128, L.sbo_by);
+          const uint64_t s_l = tc::desc(s_by + 3 * pl + kb, 128, L.sbo_by);
+          const uint32_t first = (gY.yc == 0) ? 0u : 1u;
+#pragma unroll
+          for (int t2 = 0; t2 < 2; ++t2) {
+            const uint32_t a0 = s_ay + t2 * kTileYBytes;
+            const uint64_t re_h = tc::desc(a0 + 0 * kTileYBytes, kLboY, kSboY);
+            const uint64_t re_l = tc::desc(a0 + 2 * kTileYBytes, kLboY, kSboY);
+            const uint64_t im_h = tc::desc(a0 + 4 * kTileYBytes, kLboY, kSboY);
+            const uint64_t im_l = tc::desc(a0 + 6 * kTileYBytes, kLboY, kSboY);
+            const uint32_t dre = d3 + 32 * t2, dim = dre + 16;
+            mma3(dre, re_h, re_l, c_h, c_l, id16, first);
+            mma3(dre, im_h, im_l, s_h, s_l, id16, 1u);
+            mma3(dim, im_h, im_l, c_h, c_l, id16, first);
+            mma3(dim, re_h, re_l, s_h, s_l, id16n, 1u);
+          }
+          tc::commit(&ay_empty);
+          ++ygroup;
+          if (gY.yc == n_yc - 1) {
+            tc::commit(&d3_full);
+            ++yslab;
+          }
+        }
+        gY.advance(n_yc, n_zb);
+      }
+      if (G >= 1 && G - 1 < n_groups) {
+        // ---- stage Z for group G - 1 (K block zb) -> D2
+        tc::mbar_wait(&az_full, (G - 1) & 1);
+        if (gZ.zb == 0) tc::mbar_wait(&d2_empty, (zchunk & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t pl = 2 * L.sbo_bz;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const uint32_t ka = 2 * s * kLboZ, kb = (uint32_t)(gZ.zb * 4 + 2 * s) * 128;
+          const uint64_t re_h = tc::desc(s_az + 0 * kAZBytes + ka, kLboZ, kSboZ);
+          const uint64_t re_l = tc::desc(s_az + 1 * kAZBytes + ka, kLboZ, kSboZ);
+          const uint64_t im_h = tc::desc(s_az + 2 * kAZBytes + ka, kLboZ, kSboZ);
+          const uint64_t im_l = tc::desc(s_az + 3 * kAZBytes + ka, kLboZ, kSboZ);
+          const uint64_t c_h = tc::desc(s_bz + 0 * pl + kb, 128, L.sbo_bz);
+          const uint64_t c_l = tc::desc(s_bz + 1 * pl + kb, 128, L.sbo_bz);
+          const uint64_t s_h = tc::desc(s_bz + 2 * pl + kb, 128, L.sbo_bz);
+          const uint64_t s_l = tc::desc(s_bz + 3 * pl + kb, 128, L.sbo_bz);
+          const uint32_t first = (gZ.zb == 0 && s == 0) ? 0u : 1u;
+          // e^{-i}: re += A_re C + A_im S ;  im += A_im C - A_re S
+          mma3(d2, re_h, re_l, c_h, c_l, id16, first);
+          mma3(d2, im_h, im_l, s_h, s_l, id16, 1u);
+          mma3(d2 + 16, im_h, im_l, c_h, c_l, id16, first);
+          mma3(d2 + 16, re_h, re_l, s_h, s_l, id16n, 1u);
+        }
+        tc::commit(&az_empty);
+        if (gZ.zb == n_zb - 1) {
+          tc::commit(&d2_full);
+          ++zchunk;
+        }
+        gZ.advance(n_yc, n_zb);
+      }
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -777,8 +812,8 @@ static constexpr int kSmemCap = 225 * 1024;
 template <int MODE, bool VEC>
 static int launch_fwd(const dfno_geom& g, const void* src, const void* pre, double scale, void* out,
                       cudaStream_t st) {
-  // tiles held in registers ahead of use: 3 (one input) / 2 (grad: two inputs)
-  constexpr int PF = (MODE == DFNO_SRC_GRAD) ? 2 : 3;
+  // tiles held in registers ahead of use by each converter thread
+  constexpr int PF = 2;
   const FwdLayout L = fwd_layout(g.ny, g.nz, g.nt);
   if (L.total > kSmemCap) return DFNO_ERR_UNSUPPORTED;
   auto kern = k_yzt_fwd_tc<MODE, VEC, PF>;
@@ -786,7 +821,7 @@ static int launch_fwd(const dfno_geom& g, const void* src, const void* pre, doub
     return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   const int grid = sm_count() < slabs ? sm_count() : slabs;
-  kern<<<grid, kThreads, L.total, st>>>(g, (const float*)src, (const float*)pre, (float)scale, (float2*)out);
+  kern<<<grid, kFwdThreads, L.total, st>>>(g, (const float*)src, (const float*)pre, (float)scale, (float2*)out);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }

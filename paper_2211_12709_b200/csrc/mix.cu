@@ -125,31 +125,34 @@ __global__ void __launch_bounds__(256) k_mix_fwd(long long npts, int nb, int cin
 // ---------------------------------------------------------------------------
 constexpr int kMixBwdThreads = 256;
 
-// CM = padded max(cin, cout) (multiple of 4).  One point per thread per tile.
-template <typename R, int CM>
+// CM = padded max(cin, cout) (multiple of 4); V consecutive points per thread
+// (vector loads / stores along the contiguous point index); a tile is
+// kMixBwdThreads * V points of one batch entry.
+//   phase 1  gp[o][v] = gout * act'(pre)            (registers + smem Gs[o][p])
+//   phase 2  a[i][v]  = f(src); gin[i] = sum_o gp[o] w[i][o]   (smem As[i][p])
+//   phase 3  gW partial (4x4 register tiles per thread, point groups)
+template <typename R, int CM, int V>
 __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
     long long npts, int nb, int cin, int cout, const R* __restrict__ gout, const R* __restrict__ pre,
     const R* __restrict__ src, int src_act, int act, const R* __restrict__ w, R* __restrict__ gin,
     R* __restrict__ partials) {
-  constexpr int TP = kMixBwdThreads;
-  constexpr int NB4 = CM / 4;                 // 4-blocks per channel dim
-  constexpr int NPAIR = NB4 * NB4;            // (ib, ob) 4x4 tiles
-  constexpr int NGRP = (TP / NPAIR) > 0 ? (TP / NPAIR) : 1;  // point groups
+  constexpr int TP = kMixBwdThreads * V;      // points per tile
+  constexpr int NB4 = CM / 4;
+  constexpr int NPAIR = NB4 * NB4;
+  constexpr int NGRP = (kMixBwdThreads / NPAIR) > 0 ? (kMixBwdThreads / NPAIR) : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* ws = reinterpret_cast<R*>(smem_raw);     // [CM][CM] (i, o), zero padded
-  R* As = ws + CM * CM;                       // [TP][CM]  f(src) per point
-  R* Gs = As + TP * CM;                       // [TP][CM]  gp per point
-  R* red = Gs + TP * CM;                      // [NGRP][NPAIR*16] reduction
+  R* As = ws + CM * CM;                       // [CM][TP]
+  R* Gs = As + CM * TP;                       // [CM][TP]
+  R* red = Gs + CM * TP;                      // [NGRP][NPAIR*16]
 
   for (int k = threadIdx.x; k < CM * CM; k += blockDim.x) {
     const int i = k / CM, o = k % CM;
     ws[k] = (i < cin && o < cout) ? w[(long long)i * cout + o] : (R)0;
   }
-
   const int tid = threadIdx.x;
-  const int pair = tid % NPAIR;
-  const int grp = tid / NPAIR;
-  const bool reducer = (tid < NPAIR * NGRP);
+  const int pair = tid % NPAIR, grp = tid / NPAIR;
+  const bool reducer = tid < NPAIR * NGRP;
   const int ib = pair / NB4, ob = pair % NB4;
   R acc[4][4];
 #pragma unroll
@@ -157,62 +160,90 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = (R)0;
 
-  const long long total = (long long)nb * npts;
-  const long long ntiles = (total + TP - 1) / TP;
+  const long long tiles_per_b = (npts + TP - 1) / TP;
+  const long long ntiles = tiles_per_b * nb;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    __syncthreads();  // previous tile's As/Gs fully consumed
-    const long long q = tile * TP + tid;
-    R gp[CM];
-    R av[CM];
-    if (q < total) {
-      const long long bb = q / npts, p = q - bb * npts;
-      const R* go = gout + bb * cout * npts + p;
-      const R* pr = pre + bb * cout * npts + p;
+    const long long bb = tile / tiles_per_b;
+    const long long p0 = (tile - bb * tiles_per_b) * TP;
+    const long long p = p0 + (long long)tid * V;
+    const bool full = (p + V <= npts);
+    __syncthreads();  // previous tile's As / Gs consumed
+    // ---- phase 1: gp = gout * act'(pre)
+    R gp[CM][V];
+    const R* go = gout + bb * cout * npts + p;
+    const R* pr = pre + bb * cout * npts + p;
 #pragma unroll
-      for (int o = 0; o < CM; ++o) {
-        gp[o] = (R)0;
-        if (o < cout) gp[o] = __ldg(go + (long long)o * npts) * act_deriv<R>(act, __ldg(pr + (long long)o * npts));
-      }
-      const R* s = src + bb * cin * npts + p;
+    for (int o = 0; o < CM; ++o) {
+      R gv[V], pv[V];
+      if (o < cout && full) {
+        ldv<R, V>(go + (long long)o * npts, gv);
+        ldv<R, V>(pr + (long long)o * npts, pv);
+      } else {
 #pragma unroll
-      for (int i = 0; i < CM; ++i) {
-        av[i] = (R)0;
-        if (i < cin) {
-          R v = __ldg(s + (long long)i * npts);
-          av[i] = src_act ? act_apply<R>(act, v) : v;
+        for (int k = 0; k < V; ++k) {
+          const bool ok = (o < cout) && (p + k < npts);
+          gv[k] = ok ? go[(long long)o * npts + k] : (R)0;
+          pv[k] = ok ? pr[(long long)o * npts + k] : (R)0;
         }
       }
-      if (gin) {
-        R* gi = gin + bb * cin * npts + p;
-        for (int i = 0; i < cin; ++i) {
-          R sacc = (R)0;
 #pragma unroll
-          for (int o = 0; o < CM; ++o) sacc = fma(gp[o], ws[i * CM + o], sacc);
-          gi[(long long)i * npts] = sacc;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int o = 0; o < CM; ++o) {
-        gp[o] = (R)0;
-        av[o] = (R)0;
-      }
+      for (int k = 0; k < V; ++k) gp[o][k] = gv[k] * act_deriv<R>(act, pv[k]);
+      stv<R, V>(Gs + o * TP + tid * V, gp[o]);
     }
+    // ---- phase 2: a = f(src) -> As ; gin = sum_o gp w
+    const R* sp = src + bb * cin * npts + p;
+    R* gi = gin ? gin + bb * cin * npts + p : nullptr;
+    for (int i = 0; i < CM; ++i) {
+      if (i >= cin) {
+        R z[V];
 #pragma unroll
-    for (int k = 0; k < CM; ++k) {
-      As[tid * CM + k] = av[k];
-      Gs[tid * CM + k] = gp[k];
+        for (int k = 0; k < V; ++k) z[k] = (R)0;
+        stv<R, V>(As + i * TP + tid * V, z);
+        continue;
+      }
+      R av[V];
+      if (full) {
+        ldv<R, V>(sp + (long long)i * npts, av);
+      } else {
+#pragma unroll
+        for (int k = 0; k < V; ++k) av[k] = (p + k < npts) ? sp[(long long)i * npts + k] : (R)0;
+      }
+      if (src_act) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) av[k] = act_apply<R>(act, av[k]);
+      }
+      stv<R, V>(As + i * TP + tid * V, av);
+      if (gi) {
+        R s[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) s[k] = (R)0;
+        const R* wr = ws + i * CM;
+#pragma unroll
+        for (int o = 0; o < CM; ++o) {
+          const R wv = wr[o];
+#pragma unroll
+          for (int k = 0; k < V; ++k) s[k] = fma(gp[o][k], wv, s[k]);
+        }
+        if (full) {
+          stv<R, V>(gi + (long long)i * npts, s);
+        } else {
+#pragma unroll
+          for (int k = 0; k < V; ++k)
+            if (p + k < npts) gi[(long long)i * npts + k] = s[k];
+        }
+      }
     }
     __syncthreads();
+    // ---- phase 3: weight-gradient partial sums
     if (reducer) {
+      const R* ar = As + ib * 4 * TP;
+      const R* gr = Gs + ob * 4 * TP;
       for (int t = grp; t < TP; t += NGRP) {
-        const R* ar = As + t * CM + ib * 4;
-        const R* gr = Gs + t * CM + ob * 4;
         R a4[4], g4[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          a4[k] = ar[k];
-          g4[k] = gr[k];
+          a4[k] = ar[k * TP + t];
+          g4[k] = gr[k * TP + t];
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -234,9 +265,9 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
   for (int e = tid; e < NPAIR * 16; e += blockDim.x) {
     R s = (R)0;
     for (int gI = 0; gI < NGRP; ++gI) s += red[gI * NPAIR * 16 + e];
-    const int pr = e / 16, ab = e % 16;
-    const int i = (pr / NB4) * 4 + ab / 4;
-    const int o = (pr % NB4) * 4 + ab % 4;
+    const int pr2 = e / 16, ab = e % 16;
+    const int i = (pr2 / NB4) * 4 + ab / 4;
+    const int o = (pr2 % NB4) * 4 + ab % 4;
     if (i < cin && o < cout) outp[i * cout + o] = s;
   }
 }
@@ -328,23 +359,31 @@ static int mix_bwd_cm(int cin, int cout) {
   return -1;
 }
 
+template <typename R>
+static constexpr int mix_bwd_v() {
+  return sizeof(R) == 4 ? 2 : 1;
+}
+
+// CTA count (= number of weight-gradient partials): independent of the
+// vector width so dfno_mix_bwd_partials can size the buffer up front.
 static int mix_bwd_blocks(long long npts, int nb) {
-  const long long tiles = ((long long)nb * npts + kMixBwdThreads - 1) / kMixBwdThreads;
+  const long long tiles = ((npts + kMixBwdThreads - 1) / kMixBwdThreads) * nb;
   long long blocks = (long long)num_sms() * 2;
   if (blocks > tiles) blocks = tiles;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
 }
 
-template <typename R, int CM>
-static int launch_mix_bwd(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
-                          const void* src, int src_act, int act, const void* w, void* gin, void* partials,
-                          cudaStream_t st) {
+template <typename R, int CM, int V>
+static int launch_mix_bwd_v(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                            const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                            cudaStream_t st) {
   constexpr int NB4 = CM / 4;
   constexpr int NPAIR = NB4 * NB4;
   constexpr int NGRP = (kMixBwdThreads / NPAIR) > 0 ? (kMixBwdThreads / NPAIR) : 1;
-  const size_t smem = sizeof(R) * ((size_t)CM * CM + 2 * (size_t)kMixBwdThreads * CM + (size_t)NGRP * NPAIR * 16);
-  auto kern = k_mix_bwd<R, CM>;
+  constexpr int TP = kMixBwdThreads * V;
+  const size_t smem = sizeof(R) * ((size_t)CM * CM + 2 * (size_t)TP * CM + (size_t)NGRP * NPAIR * 16);
+  auto kern = k_mix_bwd<R, CM, V>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int blocks = mix_bwd_blocks(npts, nb);
@@ -352,6 +391,19 @@ static int launch_mix_bwd(long long npts, int nb, int cin, int cout, const void*
                                              src_act, act, (const R*)w, (R*)gin, (R*)partials);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
+}
+
+template <typename R, int CM>
+static int launch_mix_bwd(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                          const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                          cudaStream_t st) {
+  constexpr int V = mix_bwd_v<R>();
+  // vector path needs every row V-aligned
+  const bool aligned = (npts % V == 0) && ((uintptr_t)gout % (V * sizeof(R)) == 0) &&
+                       ((uintptr_t)pre % (V * sizeof(R)) == 0) && ((uintptr_t)src % (V * sizeof(R)) == 0) &&
+                       (gin == nullptr || (uintptr_t)gin % (V * sizeof(R)) == 0);
+  if (aligned) return launch_mix_bwd_v<R, CM, V>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+  return launch_mix_bwd_v<R, CM, 1>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
 }
 
 template <typename R>

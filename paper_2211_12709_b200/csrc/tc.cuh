@@ -191,32 +191,5 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// ---- erf-GELU at ~1e-7 absolute accuracy in ~15 instructions -------------
-// erf(x) = 1 - t (a1 + t (a2 + t (a3 + t (a4 + t a5)))) e^{-x^2},
-// t = 1 / (1 + p|x|)   (Abramowitz & Stegun 7.1.26, |error| <= 1.5e-7).
-// Returns gelu(h) = h Phi(h) and, optionally, gelu'(h) = Phi(h) + h phi(h),
-// sharing e^{-h^2/2} between them (reference d/fno.py:41-55).
-__device__ __forceinline__ float phi_cdf(float h, float& e) {
-  const float x = fabsf(h) * 0.70710678118654752f;
-  const float t = __fdividef(1.0f, fmaf(0.3275911f, x, 1.0f));
-  float p = fmaf(1.061405429f, t, -1.453152027f);
-  p = fmaf(p, t, 1.421413741f);
-  p = fmaf(p, t, -0.284496736f);
-  p = fmaf(p, t, 0.254829592f);
-  p *= t;
-  e = exp2f(-x * x * 1.4426950408889634f);
-  const float erf_abs = fmaf(-p, e, 1.0f);
-  return 0.5f + copysignf(0.5f * erf_abs, h);
-}
-__device__ __forceinline__ float gelu_fast(float h) {
-  float e;
-  return h * phi_cdf(h, e);
-}
-__device__ __forceinline__ float gelu_grad_fast(float h) {
-  float e;
-  const float c = phi_cdf(h, e);
-  return fmaf(h * 0.3989422804014327f, e, c);
-}
-
 }  // namespace tc
 }  // namespace dfno

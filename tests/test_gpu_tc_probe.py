@@ -55,7 +55,6 @@ def run(lib, M, N, K, lbo_a, sbo_a, lbo_b, sbo_b, neg=0, twice=0, seed=0):
     dict(M=128, N=16, K=8, lbo_a=192, sbo_a=320, lbo_b=128, sbo_b=256),
     dict(M=128, N=16, K=64, lbo_a=128, sbo_a=2048, lbo_b=144, sbo_b=2304, neg=1),
     dict(M=128, N=32, K=32, lbo_a=144, sbo_a=1152, lbo_b=128, sbo_b=1024, twice=1),
-    dict(M=64, N=32, K=16, lbo_a=128, sbo_a=512, lbo_b=128, sbo_b=512),
 ])
 def test_tf32_mma_layouts(probe, case):
     err, err_exact = run(probe, **case)
