@@ -258,19 +258,33 @@ def run_ours(args):
         host = torch.empty((1, CHANNELS, xl) + grid[1:], dtype=torch.float32, pin_memory=True)
         host.copy_(x.data.cpu())
         xh = P.DenseTensor(P.DATA_LABELS, host)
-        for _ in range(2):
-            y, _, _ = step(xh)
-            float((0.5 * (y.data.double() ** 2).sum()).item())
+        # public API step loop: pinned host input staged to HBM on a copy
+        # stream (P.InputStager), step k+1's H2D overlapping step k's compute;
+        # every step's H2D and its loss read-back are inside the timed region
+        stager = P.InputStager(host.shape, torch.float32, dev)
+
+        def e2e_loop(n):
+            loss = None
+            stager.put(xh)
+            for k in range(n):
+                xin = stager.get()
+                if k + 1 < n:
+                    stager.put(xh)
+                cache = P.ForwardCache()
+                y = P.fno_forward(comm, xin, params, cfg, cache)
+                loss = 0.5 * float(torch.linalg.vector_norm(y.data, dtype=torch.float64).item()) ** 2  # D2H
+                P.fno_backward(comm, y, params, cfg, cache)
+            return loss
+
+        e2e_loop(2)
         barrier()
+        h2d0 = stager.h2d_bytes
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
         e0.record()
-        for _ in range(args.steps):
-            cache = P.ForwardCache()
-            y = P.fno_forward(comm, xh, params, cfg, cache)          # H2D inside the API
-            loss = float((0.5 * (y.data.double() ** 2).sum()).item())  # D2H of the step's result
-            P.fno_backward(comm, y, params, cfg, cache)
+        loss = e2e_loop(args.steps)
+        stager.synchronize()
         e1.record()
         barrier()
         wall = (time.perf_counter() - w0) / args.steps * 1e3
@@ -279,9 +293,10 @@ def run_ours(args):
             tt = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        e2e = {"value": round(world * 1e3 / ems, 3), "unit": "samples/s", "h2d_bytes_per_step": host.numel() * 4,
+        e2e = {"value": round(world * 1e3 / ems, 3), "unit": "samples/s", "h2d_bytes_per_step": (stager.h2d_bytes - h2d0) // args.steps,
                "d2h_bytes_per_step": 8, "ms_per_step": round(ems, 4), "wall_ms_per_step": round(wall, 4),
-               "loss": loss}
+               "loss": loss, "h2d_path": "pinned host -> HBM on a copy stream, step k+1 staged during step k "
+                                         "(P.InputStager); loss = 0.5||y||^2 read back every step"}
 
     # ---- roofline of the dominant kernel
     hbm, hbm_kind = peaks()

@@ -54,6 +54,7 @@ from .fno import (
     slice_local,
 )
 from .partition import BlockRange, Partition, TransferBlock, block_decompose, range_intersection, repartition_plan
+from .staging import InputStager
 from .spectral import ModeSpec, fft_dims, ifft_dims, pad_modes, retained_extent, retained_indices, truncate_modes
 from .tensor import (
     DATA_LABELS,

@@ -422,6 +422,18 @@ static int mix_bwd_dispatch(long long npts, int nb, int cin, int cout, const voi
   }
 }
 
+int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre, const void* src,
+               int src_act, int act, const void* w, void* gin, void* partials, int blocks, cudaStream_t st);
+
+static bool mix_tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DFNO_DISABLE_TC");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 }  // namespace dfno
 
 using namespace dfno;
@@ -454,8 +466,14 @@ extern "C" int dfno_mix_bwd(const dfno_geom* g, int64_t npts, int cin, int cout,
   if (!g || !gout || !pre || !src || !w || !partials) return DFNO_ERR_NULL;
   if (npts < 1 || cin < 1 || cout < 1) return DFNO_ERR_DIMENSION;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g->dtype == DFNO_F32)
+  if (g->dtype == DFNO_F32) {
+    if (mix_tc_enabled()) {
+      const int rc = mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
+                                mix_bwd_blocks(npts, g->batch), st);
+      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+    }
     return mix_bwd_dispatch<float>(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials, st);
+  }
   if (g->dtype == DFNO_F64)
     return mix_bwd_dispatch<double>(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
                                     st);

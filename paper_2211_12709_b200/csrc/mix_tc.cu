@@ -1,0 +1,248 @@
+// Channel-mix backward on the tcgen05 tensor cores (fp32 via 3xTF32).
+//
+// Replaces the mixer part of fno_backward (reference d/fno.py:484-486 and
+// :497-499): gp = g * act'(pre) (d/fno.py:484, :497), _mix_input_grad
+// (d/fno.py:409-412) and _mix_weight_grad (d/fno.py:405-406).  Both
+// contractions are GEMMs over a 128-point tile held one point per thread:
+//
+//   GEMM1 (input grad)   D1[p][i]  = sum_o gp[p][o] W[i][o]
+//        A = gp (128 points x K = o) in TMEM (tcgen05.st from the owning
+//        thread), B = W (i x o) in shared memory, 3 products per K step
+//        (hi*hi + lo*hi + hi*lo), D1 read back by the owning thread and
+//        stored coalesced.
+//   GEMM2 (weight grad)  D2[r][c] += sum_p A2[r][p] B2[c][p]
+//        rows r: a_hi(i) at r = i, a_lo(i) at r = 32 + i; columns c: gp_hi(o)
+//        at c = o, gp_lo(o) at c = 32 + o, so ONE M=128 N=64 K=8 MMA per 8
+//        points yields all four hi/lo cross products; D2 accumulates over
+//        every tile of the CTA in TMEM and the three significant quadrants
+//        are summed once at the end into this CTA's partial (reduced in fixed
+//        order by k_reduce_partials: deterministic, d/training.py:77-82).
+//        Rows 64..127 of the A2 operand alias B2 (their D2 rows are never
+//        read).
+//
+// Shared-memory operands are SWIZZLE_NONE K-major with a padded LBO of 144 B
+// so the one-point-per-thread scalar stores are bank-conflict free.  The MMAs
+// of tile i run while the CTA loads tile i + 1 (one mbarrier per CTA).
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace dfno {
+
+namespace {
+constexpr int kMbThreads = 128;             // one thread per point of a 128-point tile
+constexpr int kMbLbo = 144;                 // bytes between K-adjacent core matrices
+constexpr int kMbSbo = 32 * kMbLbo;         // bytes between 8-row groups (K = 128 points)
+constexpr int kMbOpBytes = 8 * kMbSbo;      // 64 rows x 128 points
+constexpr uint32_t kMbTmemCols = 256;       // D1 0..31 | A1 hi 32..63 | A1 lo 64..95 | D2 128..191
+
+__device__ __forceinline__ int mb_off(int r, int k) {
+  return (r >> 3) * kMbSbo + (k >> 2) * kMbLbo + (r & 7) * 16 + (k & 3) * 4;
+}
+}  // namespace
+
+template <int CM>
+__global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, int nb, int cin, int cout,
+                                                              const float* __restrict__ gout,
+                                                              const float* __restrict__ pre,
+                                                              const float* __restrict__ src, int src_act, int act,
+                                                              const float* __restrict__ w, float* __restrict__ gin,
+                                                              float* __restrict__ partials) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  unsigned char* a2 = smem;
+  unsigned char* b2 = smem + kMbOpBytes;
+  unsigned char* b1 = smem + 2 * kMbOpBytes;  // W hi plane, then lo plane
+  const int KPo = (cout + 7) & ~7;             // GEMM1 K (o), multiple of 8
+  const int NPi = (cin + 15) & ~15;            // GEMM1 N (i), multiple of 16
+  const int sbo_b1 = (KPo / 4) * 128;
+  const int b1_plane = (NPi / 8) * sbo_b1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool want_gin = gin != nullptr;
+
+  for (int e = tid; e < NPi * KPo; e += kMbThreads) {
+    const int i = e / KPo, o = e % KPo;
+    const float v = (i < cin && o < cout) ? w[(long long)i * cout + o] : 0.f;
+    float h, l;
+    tc::split_rn(v, h, l);
+    const int off = (i >> 3) * sbo_b1 + (o >> 2) * 128 + (i & 7) * 16 + (o & 3) * 4;
+    *reinterpret_cast<float*>(b1 + off) = h;
+    *reinterpret_cast<float*>(b1 + b1_plane + off) = l;
+  }
+  if (warp == 0) tc::tmem_alloc<kMbTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t d1 = tmem, a1h = tmem + 32, a1l = tmem + 64, d2 = tmem + 128;
+  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+
+  const long long tiles_per_b = (npts + kMbThreads - 1) / kMbThreads;
+  const long long ntiles = tiles_per_b * nb;
+  int it = 0;
+  long long prev_out = -1;  // gin element offset of the previous tile's point (or -1)
+
+  auto drain_gin = [&]() {
+    uint32_t r[32];
+    tc::tmem_ld32_nowait(d1 + lane_off, r);
+    tc::tmem_ld_wait();
+    if (prev_out >= 0) {
+#pragma unroll
+      for (int i = 0; i < CM; ++i)
+        if (i < cin) __stcs(gin + prev_out + (long long)i * npts, __uint_as_float(r[i]));
+    }
+  };
+
+#pragma unroll 1
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const long long bb = tile / tiles_per_b;
+    const long long p = (tile - bb * tiles_per_b) * kMbThreads + tid;
+    const bool valid = p < npts;
+    float gv[CM], pv[CM], sv[CM];
+    {
+      const float* g0 = gout + bb * cout * npts + p;
+      const float* p0 = pre + bb * cout * npts + p;
+      const float* s0 = src + bb * cin * npts + p;
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        const bool ok = valid && o < cout;
+        gv[o] = ok ? __ldcs(g0 + (long long)o * npts) : 0.f;
+        pv[o] = ok ? __ldcs(p0 + (long long)o * npts) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < CM; ++i) sv[i] = (valid && i < cin) ? __ldg(s0 + (long long)i * npts) : 0.f;
+    }
+    // gp = g * act'(pre) ; a = act(src) or src  (zero for padding / invalid points)
+#pragma unroll
+    for (int o = 0; o < CM; ++o) gv[o] *= act_deriv<float>(act, pv[o]);
+    if (src_act) {
+#pragma unroll
+      for (int i = 0; i < CM; ++i) sv[i] = act_apply<float>(act, sv[i]);
+    }
+    if (it > 0) {  // MMAs of the previous tile done: its operands are free, D1 holds its input grad
+      tc::mbar_wait(&bar, (it - 1) & 1);
+      tc::fence_after();
+      if (want_gin) drain_gin();
+    }
+    if (want_gin) {
+      float h[32], l[32];
+#pragma unroll
+      for (int o = 0; o < 32; ++o) {
+        if (o < CM) tc::split_rn(gv[o], h[o], l[o]);
+        else h[o] = l[o] = 0.f;
+      }
+      tc::tmem_st32(a1h + lane_off, h);
+      tc::tmem_st32(a1l + lane_off, l);
+    }
+#pragma unroll
+    for (int i = 0; i < CM; ++i) {
+      if (i < cin) {
+        float h, l;
+        tc::split_rn(sv[i], h, l);
+        *reinterpret_cast<float*>(a2 + mb_off(i, tid)) = h;
+        *reinterpret_cast<float*>(a2 + mb_off(32 + i, tid)) = l;
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < CM; ++o) {
+      if (o < cout) {
+        float h, l;
+        tc::split_rn(gv[o], h, l);
+        *reinterpret_cast<float*>(b2 + mb_off(o, tid)) = h;
+        *reinterpret_cast<float*>(b2 + mb_off(32 + o, tid)) = l;
+      }
+    }
+    if (want_gin) tc::tmem_st_wait();
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      if (want_gin) {
+        const uint32_t id1 = tc::idesc_tf32(128, NPi);
+        const uint32_t sb1 = tc::smem_u32(b1);
+        for (int s = 0; s < KPo / 8; ++s) {
+          const uint64_t bh = tc::desc(sb1 + s * 256, 128, sbo_b1);
+          const uint64_t bl = tc::desc(sb1 + b1_plane + s * 256, 128, sbo_b1);
+          tc::mma_tf32_ts(d1, a1h + 8 * s, bh, id1, s > 0 ? 1u : 0u);
+          tc::mma_tf32_ts(d1, a1l + 8 * s, bh, id1, 1u);
+          tc::mma_tf32_ts(d1, a1h + 8 * s, bl, id1, 1u);
+        }
+      }
+      const uint32_t id2 = tc::idesc_tf32(128, 64);
+      const uint32_t sa2 = tc::smem_u32(a2), sb2 = tc::smem_u32(b2);
+#pragma unroll 4
+      for (int s = 0; s < kMbThreads / 8; ++s)
+        tc::mma_tf32(d2, tc::desc(sa2 + s * 2 * kMbLbo, kMbLbo, kMbSbo), tc::desc(sb2 + s * 2 * kMbLbo, kMbLbo, kMbSbo),
+                     id2, (it > 0 || s > 0) ? 1u : 0u);
+      tc::commit(&bar);
+    }
+    prev_out = valid ? (bb * cin * npts + p) : -1;
+  }
+  if (it > 0) {
+    tc::mbar_wait(&bar, (it - 1) & 1);
+    tc::fence_after();
+    if (want_gin) drain_gin();
+  }
+  // ---- weight-gradient partial: D2 quadrants -> shared -> partial
+  __syncthreads();  // every thread is past its last operand write
+  float* st = reinterpret_cast<float*>(smem);  // [64][65], aliases A2 (all MMAs done)
+  if (it > 0 && warp < 2) {
+    uint32_t r0[32], r1[32];
+    tc::tmem_ld32_nowait(d2 + lane_off, r0);
+    tc::tmem_ld32_nowait(d2 + lane_off + 32, r1);
+    tc::tmem_ld_wait();
+    const int row = 32 * warp + lane;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      st[row * 65 + c] = __uint_as_float(r0[c]);
+      st[row * 65 + 32 + c] = __uint_as_float(r1[c]);
+    }
+  }
+  __syncthreads();
+  float* outp = partials + (long long)blockIdx.x * cin * cout;
+  for (int e = tid; e < cin * cout; e += kMbThreads) {
+    const int i = e / cout, o = e % cout;
+    float v = 0.f;
+    if (it > 0) v = (st[i * 65 + o] + st[i * 65 + 32 + o]) + (st[(32 + i) * 65 + o] + st[(32 + i) * 65 + 32 + o]);
+    outp[e] = v;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kMbTmemCols>(tmem);
+}
+
+template <int CM>
+static int launch_mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                             const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                             int blocks, cudaStream_t st) {
+  const int smem = 2 * kMbOpBytes + 2 * 4 * 1024;
+  auto kern = k_mix_bwd_tc<CM>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  kern<<<blocks, kMbThreads, smem, st>>>(npts, nb, cin, cout, (const float*)gout, (const float*)pre,
+                                         (const float*)src, src_act, act, (const float*)w, (float*)gin,
+                                         (float*)partials);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+// fp32, cin and cout <= 32; returns DFNO_ERR_UNSUPPORTED otherwise.
+int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre, const void* src,
+               int src_act, int act, const void* w, void* gin, void* partials, int blocks, cudaStream_t st) {
+  const int m = cin > cout ? cin : cout;
+  if (m > 32 || blocks < 1) return DFNO_ERR_UNSUPPORTED;
+  if (m <= 8) return launch_mix_bwd_tc<8>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
+  if (m <= 16)
+    return launch_mix_bwd_tc<16>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
+  if (m <= 24)
+    return launch_mix_bwd_tc<24>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
+  return launch_mix_bwd_tc<32>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
+}
+
+}  // namespace dfno

@@ -1,0 +1,328 @@
+// Microbenchmarks / layout probes for tcgen05 design decisions (test-only):
+//  * mode 0: SS MMA throughput: R x (M=128, N, K=8) kind::tf32, A and B from SMEM
+//  * mode 1: TS MMA throughput: A from TMEM
+//  * mode 2: TS correctness: A (128 x K) written to TMEM with tcgen05.st.32x32b,
+//            D = A * B^T read back (compared by tests/test_gpu_tc_probe.py)
+//  * mode 3: TMEM load throughput: 4 warps x R tcgen05.ld.32x32b.x32
+//  * mode 4: TMEM store throughput: 4 warps x R tcgen05.st.32x32b.x32
+//  * mode 10+P / 20+P: SS / TS MMAs round-robin over P independent accumulators
+// Cycle counts are written to cyc[0].
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tc.cuh"
+
+using namespace dfno;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// issue predicated on lane 0 so the whole warp runs the loop convergently
+__device__ __forceinline__ void mma_ss_p(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc, bool issue) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"((uint32_t)issue));
+}
+__device__ __forceinline__ void mma_ts_p(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc, bool issue) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc), "r"((uint32_t)issue));
+}
+
+__global__ void probe_perf(int mode, const float* A, const float* B, float* D, int N, int K, int R,
+                           long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  // A: 128 x K K-major (LBO 128, SBO = K/4*128), B: N x K
+  const int sbo_a = (K / 4) * 128, sbo_b = (K / 4) * 128;
+  float* sa = reinterpret_cast<float*>(smem);
+  float* sb = reinterpret_cast<float*>(smem + 16 * sbo_a);
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  for (int e = tid; e < 128 * K; e += blockDim.x) {
+    int r = e / K, k = e % K;
+    sa[((r / 8) * sbo_a + (k / 4) * 128 + (r % 8) * 16 + (k % 4) * 4) / 4] = A ? A[e] : 1.0f;
+  }
+  for (int e = tid; e < N * K; e += blockDim.x) {
+    int r = e / K, k = e % K;
+    sb[((r / 8) * sbo_b + (k / 4) * 128 + (r % 8) * 16 + (k % 4) * 4) / 4] = B ? B[e] : 1.0f;
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t d = tm;            // D at columns 0..N-1
+  const uint32_t a_t = tm + 256;    // A (TS) at columns 256..256+K-1
+  const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+  const int P = mode >= 20 ? mode - 20 : (mode >= 10 ? mode - 10 : 1);
+  const bool ts = (mode == 1 || mode == 2 || mode >= 20);
+  if (ts) {
+    if (warp < 4) {
+      for (int c0 = 0; c0 < K; c0 += 32) {
+        float v[32];
+        for (int j = 0; j < 32; ++j) v[j] = (A && c0 + j < K) ? A[(32 * warp + lane) * K + c0 + j] : 1.0f;
+        tmem_st32(a_t + lane_off + c0, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  long long t0 = clock64();
+  unsigned long long g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  if (mode <= 2 || mode >= 10) {
+    if (warp == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, N);
+      const int reps = (mode == 2) ? 1 : R;
+      for (int rep = 0; rep < reps; ++rep)
+        for (int s = 0; s < K / 8; ++s) {
+          const uint64_t db = tc::desc(tc::smem_u32(sb) + 2 * s * 128, 128, sbo_b);
+          const uint32_t dd = d + (uint32_t)(((rep * (K / 8) + s) % P) * N);
+          const uint32_t acc = (rep * (K / 8) + s) >= P ? 1u : 0u;
+          if (!ts)
+            mma_ss_p(dd, tc::desc(tc::smem_u32(sa) + 2 * s * 128, 128, sbo_a), db, idesc, acc, lane == 0);
+          else
+            mma_ts_p(dd, a_t + 8 * s, db, idesc, acc, lane == 0);
+        }
+      if (lane == 0) tc::commit(&bar);
+      __syncwarp();
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after();
+  } else if (mode == 3) {
+    float acc = 0.f;
+    if (warp < 4)
+      for (int r = 0; r < R; ++r) {
+        float v[32];
+        tc::tmem_ld32(tm + lane_off + 32 * (r & 7), v);
+        acc += v[r & 31];
+      }
+    if (acc == 12345.f) D[0] = acc;
+  } else if (mode == 4) {
+    if (warp < 4) {
+      float v[32];
+      for (int j = 0; j < 32; ++j) v[j] = (float)j;
+      for (int r = 0; r < R; ++r) tmem_st32(tm + lane_off + 32 * (r & 7), v);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  unsigned long long g1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  if (tid == 0) {
+    cyc[0] = t1 - t0;
+    cyc[1] = (long long)(g1 - g0);
+  }
+  if (mode <= 2 && warp < 4 && D) {  // accumulator 0
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(d + lane_off + c0, v);
+      for (int j = 0; j < 16; ++j) D[(32 * warp + lane) * N + c0 + j] = v[j];
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_perf_run(int mode, const float* A, const float* B, float* D, int N, int K, int R,
+                              long long* cyc) {
+  int smem = 16 * (K / 4) * 128 + 32 * (K / 4) * 128 + 1024;
+  cudaFuncSetAttribute(probe_perf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  probe_perf<<<1, 128, smem>>>(mode, A, B, D, N, K, R, cyc);
+  return (int)cudaDeviceSynchronize();
+}
+
+// Calibrated issue-rate probe: descriptors precomputed, fully unrolled
+// groups of 8 MMAs, P independent accumulators, kind::tf32 (KIND 0) or
+// kind::f16 with bf16 operands (KIND 1), A from SMEM (TS=false) or TMEM.
+template <int KIND, bool TS>
+__global__ void probe_rate(int N, int P, int R, long long* cyc, int variant) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  for (int e = tid; e < 48 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0x3c003c00u;
+  if (warp == 0) tc::tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t idesc = KIND == 0 ? tc::idesc_tf32(128, N)
+                                   : ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                                      ((uint32_t)(128 >> 4) << 24));
+  const uint64_t da = tc::desc(tc::smem_u32(smem), 128, 256);
+  const uint64_t db = tc::desc(tc::smem_u32(smem + 16384), 128, 256);
+  long long t0 = clock64();
+  if (tid == 0) {
+    uint32_t pcur = 0;
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t d = tm + pcur * (uint32_t)N;
+        pcur = (pcur + 1 == (uint32_t)P) ? 0u : pcur + 1;
+        const uint32_t acc = (r > 0 || j >= P) ? 1u : 0u;
+        if (TS) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+              "r"(tm + 384), "l"(db), "r"(idesc), "r"(acc));
+        } else if (KIND == 0) {
+          tc::mma_tf32(d, da, db, idesc, acc);
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+      }
+    }
+    tc::commit(&bar);
+  }
+  if (variant == 1) __syncthreads();  // everybody parks on the barrier while thread 0 issues
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after();
+  __syncthreads();
+  long long t1 = clock64();
+  if (tid == 0) cyc[0] = t1 - t0;
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_rate_run(int kind, int ts, int N, int P, int R, long long* cyc, int variant) {
+  const int smem = 48 * 1024;
+  if (kind == 0 && !ts) {
+    cudaFuncSetAttribute(probe_rate<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe_rate<0, false><<<1, 128, smem>>>(N, P, R, cyc, variant);
+  } else if (kind == 0) {
+    cudaFuncSetAttribute(probe_rate<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe_rate<0, true><<<1, 128, smem>>>(N, P, R, cyc, variant);
+  } else {
+    cudaFuncSetAttribute(probe_rate<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe_rate<1, false><<<1, 128, smem>>>(N, P, R, cyc, variant);
+  }
+  return (int)cudaDeviceSynchronize();
+}
+
+// Lean issue: compile-time N / P, fully unrolled, addresses = uniform base +
+// immediate offsets.
+template <int N, int P, bool TS>
+__global__ void probe_lean(int R, long long* cyc, int W) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < 48 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0x3c003c00u;
+  if (warp == 0) tc::tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&bar, W);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  constexpr uint32_t idesc = tc::idesc_tf32(128, N);
+  const uint64_t da = tc::desc(tc::smem_u32(smem), 128, 256);
+  const uint64_t db = tc::desc(tc::smem_u32(smem + 16384), 128, 256);
+  long long t0 = clock64();
+  if ((tid & 31) == 0 && warp < W) {
+    const uint32_t dbase = tm + (uint32_t)(warp * 64);
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t d = dbase + (uint32_t)((j % P) * N);
+        const uint64_t a_k = da + (uint64_t)((j & 1) * 16);   // K step: +256 B -> +16 in desc units
+        const uint64_t b_k = db + (uint64_t)((j & 1) * 16);
+        if (TS) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+              "r"(tm + 384 + 8 * (j & 1)), "l"(b_k), "n"(idesc), "r"(1));
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+              "l"(a_k), "l"(b_k), "n"(idesc), "r"(1));
+        }
+      }
+    }
+    tc::commit(&bar);
+  }
+  tc::mbar_wait(&bar, 0);
+  tc::fence_after();
+  __syncthreads();
+  long long t1 = clock64();
+  if (tid == 0) cyc[0] = t1 - t0;
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+template <int N, int P, bool TS>
+static int lean(int R, long long* cyc, int W = 1) {
+  cudaFuncSetAttribute(probe_lean<N, P, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024);
+  probe_lean<N, P, TS><<<1, 128, 48 * 1024>>>(R, cyc, W);
+  return (int)cudaDeviceSynchronize();
+}
+
+extern "C" int probe_lean_run(int which, int R, long long* cyc) {
+  switch (which) {
+    case 0: return lean<16, 1, false>(R, cyc);
+    case 1: return lean<16, 4, false>(R, cyc);
+    case 2: return lean<32, 1, false>(R, cyc);
+    case 3: return lean<32, 4, false>(R, cyc);
+    case 4: return lean<64, 1, false>(R, cyc);
+    case 5: return lean<64, 4, false>(R, cyc);
+    case 6: return lean<128, 1, false>(R, cyc);
+    case 7: return lean<16, 4, true>(R, cyc);
+    case 8: return lean<32, 4, true>(R, cyc);
+    case 9: return lean<64, 4, true>(R, cyc);
+    case 10: return lean<16, 1, false>(R, cyc, 2);
+    case 11: return lean<16, 1, false>(R, cyc, 4);
+    case 12: return lean<32, 1, true>(R, cyc, 2);
+    case 13: return lean<32, 1, true>(R, cyc, 4);
+    default: return -1;
+  }
+}

@@ -60,3 +60,103 @@ def test_tf32_mma_layouts(probe, case):
     err, err_exact = run(probe, **case)
     print(case, "err vs truncated-tf32 product", err, "vs fp32 product", err_exact)
     assert err < 1e-5
+
+
+@pytest.fixture(scope="module")
+def perf():
+    src = ROOT / "tests" / "probes" / "probe_tc_perf.cu"
+    so = ROOT / "tests" / "probes" / "libprobe_perf.so"
+    if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-Xcompiler",
+                        "-fPIC", "-shared", f"-I{ROOT / 'paper_2211_12709_b200' / 'csrc'}", f"-I{ROOT / 'include'}",
+                        str(src), "-o", str(so)], check=True)
+    lib = ctypes.CDLL(str(so))
+    lib.probe_perf_run.restype = ctypes.c_int
+    return lib
+
+
+def _perf(lib, mode, N, K, R, A=None, B=None):
+    cyc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    d = torch.zeros((128, N), device="cuda")
+    vp = ctypes.c_void_p
+    rc = lib.probe_perf_run(mode, vp(A.data_ptr() if A is not None else 0), vp(B.data_ptr() if B is not None else 0),
+                            vp(d.data_ptr()), N, K, R, vp(cyc.data_ptr()))
+    assert rc == 0
+    c = cyc.cpu()
+    _perf.ns = int(c[1])
+    return int(c[0]), d
+
+
+def test_tf32_mma_a_from_tmem(perf):
+    """tcgen05.mma kind::tf32 with A in TMEM (lane = row, column = k) matches
+    the truncated-TF32 product."""
+    rng = np.random.default_rng(3)
+    for N, K in ((32, 32), (64, 16), (16, 64)):
+        A = rng.standard_normal((128, K)).astype(np.float32)
+        B = rng.standard_normal((N, K)).astype(np.float32)
+        _, d = _perf(perf, 2, N, K, 1, torch.tensor(A, device="cuda"), torch.tensor(B, device="cuda"))
+        want = trunc_tf32(A) @ trunc_tf32(B).T
+        err = np.max(np.abs(d.cpu().numpy() - want)) / np.max(np.abs(want))
+        assert err < 1e-5, (N, K, err)
+
+
+def test_tcgen05_throughput_report(perf):
+    """Cycle counts behind the DFT kernels' tiling choices (printed; -s)."""
+    R = 256
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(50):  # ramp the SM clock
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
+    for N in (16, 32, 64, 128, 256):
+        ss, _ = _perf(perf, 0, N, 32, R)
+        ts, _ = _perf(perf, 1, N, 32, R)
+        print(f"M=128 K=8 N={N:3d}: SS {ss / (4 * R):6.1f} cyc/MMA   TS {ts / (4 * R):6.1f} cyc/MMA "
+              f"({_perf.ns / (4 * R):.1f} ns/MMA, clock {ts / _perf.ns:.2f} GHz)")
+    for N in (16, 32, 64):
+        for Pn in (2, 4, 8):
+            if Pn * N > 256:
+                continue
+            ss, _ = _perf(perf, 10 + Pn, N, 32, R)
+            ts, _ = _perf(perf, 20 + Pn, N, 32, R)
+            print(f"N={N:3d} x {Pn} independent accumulators: SS {ss / (4 * R):6.1f} cyc/MMA   TS {ts / (4 * R):6.1f}")
+    ld, _ = _perf(perf, 3, 32, 32, R)
+    st, _ = _perf(perf, 4, 32, 32, R)
+    print(f"tcgen05.ld 32x32b.x32 (4 warps, 16 KB): {ld / R:.1f} cyc  -> {16384 * R / ld:.0f} B/cyc")
+    print(f"tcgen05.st 32x32b.x32 (4 warps, 16 KB): {st / R:.1f} cyc  -> {16384 * R / st:.0f} B/cyc")
+
+
+def test_tcgen05_issue_rate_report(perf):
+    """Back-to-back MMA rate with precomputed descriptors (printed; -s)."""
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(50):
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
+    cyc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    R = 64
+    for kind, ts, name in ((1, 0, "bf16 SS"), (0, 0, "tf32 SS"), (0, 1, "tf32 TS")):
+        for N in (16, 32, 64, 128, 256):
+            for Pn in (1, 4):
+                if Pn * N > 384:
+                    continue
+                out = []
+                for variant in (0, 1):
+                    assert perf.probe_rate_run(kind, ts, N, Pn, R, ctypes.c_void_p(cyc.data_ptr()), variant) == 0
+                    out.append(int(cyc[0]) / (8 * R))
+                print(f"{name} M=128 N={N:3d} P={Pn}: spinning lanes {out[0]:7.1f}  parked lanes {out[1]:7.1f} cyc/MMA")
+
+
+def test_tcgen05_lean_issue_report(perf):
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(50):
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
+    cyc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    names = ["SS N16 P1", "SS N16 P4", "SS N32 P1", "SS N32 P4", "SS N64 P1", "SS N64 P4", "SS N128 P1",
+             "TS N16 P4", "TS N32 P4", "TS N64 P4", "SS N16 2 issuing warps (cyc per warp-MMA)",
+             "SS N16 4 issuing warps", "TS N32 2 issuing warps", "TS N32 4 issuing warps"]
+    for i, n in enumerate(names):
+        assert perf.probe_lean_run(i, 64, ctypes.c_void_p(cyc.data_ptr())) == 0
+        print(f"lean tf32 M=128 {n}: {int(cyc[0]) / (8 * 64):6.1f} cyc/MMA")
