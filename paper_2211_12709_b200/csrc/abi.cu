@@ -17,6 +17,8 @@ int xspec_bwd_simt(const dfno_geom&, const void*, const void*, const void*, void
 // when the geometry is outside its envelope.
 int yzt_fwd_tc(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
 int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
+// TMEM-operand tcgen05 path (dft_fwd_tc.cu)
+int yzt_fwd_tc2(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
 }  // namespace dfno
 
 using namespace dfno;
@@ -35,6 +37,11 @@ bool check_blocks(const int32_t* starts, int extent, int P) {
     cur += base + (r < rem ? 1 : 0);
   }
   return starts[P] == extent;
+}
+
+bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
 }
 
 // Environment switch for A/B measurements: DFNO_DISABLE_TC=1 forces SIMT.
@@ -115,6 +122,11 @@ extern "C" int dfno_dft_yzt_fwd(const dfno_geom* g, const void* src, const void*
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) {
     if (tc_enabled()) {
+      static const bool v1 = env_flag("DFNO_YZT_V1");  // A/B switch: previous SMEM-operand kernel
+      if (!v1) {
+        rc = yzt_fwd_tc2(*g, src, pre, src_mode, scale, xk_out, st);
+        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+      }
       rc = yzt_fwd_tc(*g, src, pre, src_mode, scale, xk_out, st);
       if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     }

@@ -1,0 +1,537 @@
+// Truncated forward (y, z, t) DFT of one rank's x-slab on the tcgen05 tensor
+// cores: every contraction runs with its data operand A in TENSOR MEMORY
+// (tcgen05.mma ... [d], [a_tmem], b_desc) so the tensor core never re-reads
+// the data from shared memory, the twiddles are the small B operand in shared
+// memory, and fp32 accuracy comes from 3xTF32 (hi*hi + lo*hi + hi*lo).
+//
+// Replaces fft_dims(a, (y,z,t)) + truncate_modes (reference d/fno.py:328-329;
+// the backward use d/fno.py:446-448 with scale 1/N_yzt).  Output is written
+// straight into the peer-major XK exchange layout (include/dfno.h).
+//
+// Per slab (b, c, x) the input [Ny][Nz][Nt] is walked in groups
+// (y chunk of 8, z block of 16) of 128 rows (y, z) x 32 t tiles:
+//
+//   TMA producer   4-D tensor-map loads (SWIZZLE_128B) of each tile into a
+//                  shared-memory ring (src, and pre in backward mode)
+//   converters     warps 0-3, thread = tile row (y, z): 8 conflict-free
+//                  LDS.128 of its 32 t, act / grad * act' fused, TF32 hi/lo
+//                  split, tcgen05.st into A_T (TMEM lane = row, column = t)
+//   MMA T          D1[(y,z)][kt re|im]   = A_T . [C | -S]_t            N=32
+//   transposers    warps 4-7: D1 -> registers -> per-warp 16x16 shared
+//                  transpose -> A_Z[(y,kt)][(re|im, z)] (same TMEM quarter)
+//   MMA Z          D2[(y,kt)][kz re|im] += A_Z . [[C,S];[-S,C]]_z      N=32
+//                  (accumulated over the z blocks of a y chunk)
+//   transposers    D2 -> shared stash -> A_Y[(kz,kt)][(re|im, y)] (2 tiles)
+//   MMA Y          D3[(kz,kt)][ky re|im] += A_Y . [[C,S];[-S,C]]_y     N=32
+//                  (accumulated over the y chunks of the slab)
+//   transposers    D3 -> XK exchange buffer (coalesced float2 stores)
+//
+// Each hand-off is an mbarrier full/empty pair; A_T, D1, A_Z, D2 are double
+// buffered; two issuing threads (stage T; stages Z + Y) keep the tensor pipe
+// fed (a single tcgen05.mma issue costs ~50 cycles, measured by
+// tests/test_gpu_tc_probe.py).  TMEM: 512 columns, one CTA per SM, persistent
+// over slabs.
+//
+// Envelope: fp32, r_y, r_z, r_t <= 16, Nt % 4 == 0 (TMA stride rule), 16-byte
+// aligned inputs; the caller falls back to dft_yzt_tc.cu otherwise.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace dfno {
+
+namespace {
+
+constexpr int kConv = 4, kTrans = 4;
+constexpr int kWarps = kConv + kTrans + 3;  // + TMA producer, MMA-T issuer, MMA-ZY issuer
+constexpr int kThreads2 = kWarps * 32;
+constexpr int kTileBytes = 128 * 32 * 4;     // 128 rows x 32 t fp32
+constexpr int kScratchWarp = 2 * 2 * 16 * 17 * 4;   // [part][yy][kt][z (+1)]
+constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
+
+// TMEM column map
+constexpr uint32_t cAT = 0, cD1 = 128, cAZ = 192, cD2 = 320, cAY = 384, cD3 = 448;
+
+struct Lay {
+  int nyc, nzb, ntb;            // y chunks (8), z blocks (16), t blocks (32)
+  int kt_tot, kz_tot, ky_tot;   // K extents of the twiddle operands
+  int sbo_t, sbo_z, sbo_y;
+  int off_ring, off_bt, off_bz, off_by, off_scr, off_stash, total;
+  int stages, srcs;             // ring depth, tiles per stage (1 or 2)
+};
+
+__host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int smem_cap) {
+  Lay L;
+  L.nyc = (ny + 7) / 8;
+  L.nzb = (nz + 15) / 16;
+  L.ntb = (nt + 31) / 32;
+  L.kt_tot = L.ntb * 32;
+  L.kz_tot = L.nzb * 32;
+  L.ky_tot = L.nyc * 16;
+  L.sbo_t = (L.kt_tot / 4) * 128;
+  L.sbo_z = (L.kz_tot / 4) * 128;
+  L.sbo_y = (L.ky_tot / 4) * 128;
+  L.srcs = srcs;
+  int o = 0;
+  L.off_bt = o; o += 2 * 4 * L.sbo_t;   // hi, lo planes of 32 rows
+  L.off_bz = o; o += 2 * 4 * L.sbo_z;
+  L.off_by = o; o += 2 * 4 * L.sbo_y;
+  L.off_scr = o; o += kTrans * kScratchWarp;
+  L.off_stash = o; o += kStashBytes;
+  o = (o + 1023) & ~1023;
+  L.off_ring = o;
+  const int stage = srcs * kTileBytes;
+  int s = (smem_cap - o) / stage;
+  if (s > 4) s = 4;
+  L.stages = s;
+  L.total = o + (s > 0 ? s : 0) * stage;
+  return L;
+}
+
+__device__ __forceinline__ int kmaj32(int r, int k, int sbo) {
+  return (r >> 3) * sbo + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+}
+
+__device__ __forceinline__ void put_split(unsigned char* b, int plane, int off, double v) {
+  const float hi = tc::round_tf32((float)v);
+  const float lo = tc::round_tf32((float)(v - (double)hi));
+  *reinterpret_cast<float*>(b + off) = hi;
+  *reinterpret_cast<float*>(b + plane + off) = lo;
+}
+
+__device__ __forceinline__ void cs(int k, int n, int N, int m, int r, double& c, double& s) {
+  c = s = 0.0;
+  if (k < r && n < N) {
+    const long long idx = ((long long)mode_freq(k, N, m) * n) % N;
+    sincospi(2.0 * (double)idx / N, &s, &c);
+  }
+}
+
+template <int MODE, int ACT>
+__device__ __forceinline__ float conv(float v, float p) {
+  if (MODE == DFNO_SRC_ACT) return act_apply<float>(ACT, v);
+  if (MODE == DFNO_SRC_GRAD) return v * act_deriv<float>(ACT, p);
+  return v;
+}
+
+}  // namespace
+
+template <int MODE, int ACT>
+__global__ void __launch_bounds__(kThreads2, 1)
+    k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
+                  const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap) {
+  constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[4], empty[4], at_full[2], at_empty[2], d1_full[2], d1_empty[2];
+  __shared__ uint64_t az_full[2], az_empty[2], d2_full[2], d2_empty[2], ay_full, ay_empty, d3_full, d3_empty;
+  __shared__ uint32_t tmem_base;
+
+  const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
+  const int XL = x_local(g);
+  const Lay L = make_lay(Ny, Nz, Nt, GRAD ? 2 : 1, smem_cap);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned char* bt = smem + L.off_bt;
+  unsigned char* bz = smem + L.off_bz;
+  unsigned char* by = smem + L.off_by;
+
+  // ---- twiddle operands (hi / lo planes, K-major, 32 rows) ---------------
+  {
+    const int pl = 4 * L.sbo_t;  // t: rows 0-15 cos(kt), 16-31 -sin(kt); K = t
+    for (int e = tid; e < 32 * L.kt_tot; e += blockDim.x) {
+      const int n = e / L.kt_tot, t = e % L.kt_tot;
+      double c, s;
+      cs(n & 15, t, Nt, g.mt, g.rt, c, s);
+      put_split(bt, pl, kmaj32(n, t, L.sbo_t), n < 16 ? c : -s);
+    }
+  }
+  {
+    // z / y: realified complex e^{-i}: K = (block, part, index); rows 0-15 out
+    // re (C on re, S on im), rows 16-31 out im (-S on re, C on im)
+    const int plz = 4 * L.sbo_z;
+    for (int e = tid; e < 32 * L.kz_tot; e += blockDim.x) {
+      const int n = e / L.kz_tot, k = e % L.kz_tot;
+      const int z = (k / 32) * 16 + (k & 15), part = (k >> 4) & 1;
+      double c, s;
+      cs(n & 15, z, Nz, g.mz, g.rz, c, s);
+      const double v = (n < 16) ? (part ? s : c) : (part ? c : -s);
+      put_split(bz, plz, kmaj32(n, k, L.sbo_z), v);
+    }
+    const int ply = 4 * L.sbo_y;
+    for (int e = tid; e < 32 * L.ky_tot; e += blockDim.x) {
+      const int n = e / L.ky_tot, k = e % L.ky_tot;
+      const int y = (k / 16) * 8 + (k & 7), part = (k >> 3) & 1;
+      double c, s;
+      cs(n & 15, y, Ny, g.my, g.ry, c, s);
+      const double v = (n < 16) ? (part ? s : c) : (part ? c : -s);
+      put_split(by, ply, kmaj32(n, k, L.sbo_y), v);
+    }
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  if (tid == 0) {
+    for (int s = 0; s < 4; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], kConv * 32);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&at_full[b], kConv * 32);
+      tc::mbar_init(&at_empty[b], 1);
+      tc::mbar_init(&d1_full[b], 1);
+      tc::mbar_init(&d1_empty[b], kTrans * 32);
+      tc::mbar_init(&az_full[b], kTrans * 32);
+      tc::mbar_init(&az_empty[b], 1);
+      tc::mbar_init(&d2_full[b], 1);
+      tc::mbar_init(&d2_empty[b], kTrans * 32);
+    }
+    tc::mbar_init(&ay_full, kTrans * 32);
+    tc::mbar_init(&ay_empty, 1);
+    tc::mbar_init(&d3_full, 1);
+    tc::mbar_init(&d3_empty, kTrans * 32);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  const int slabs = g.batch * g.c * XL;
+  const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int groups_per_slab = L.nyc * L.nzb;
+  const int n_groups = my_slabs * groups_per_slab;
+  const int n_tiles = n_groups * L.ntb;
+  const int S = L.stages;
+
+  if (warp == kConv + kTrans) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&tm_src);
+      if (GRAD) tc::tma_prefetch_desc(&tm_pre);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % S, n = i / S;
+        const int tb = i % L.ntb, gi = i / L.ntb;
+        const int slab = (int)blockIdx.x + (gi / groups_per_slab) * (int)gridDim.x;
+        const int gr = gi % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
+        tc::mbar_wait(&empty[s], (n & 1) ^ 1);
+        tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
+        unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
+        tc::tma_load_4d(dst, &tm_src, tb * 32, zb * 16, yc * 8, slab, &full[s]);
+        if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, zb * 16, yc * 8, slab, &full[s]);
+      }
+    }
+  } else if (warp < kConv) {
+    // ======================= converters =======================
+    const int r = tid;  // tile row = (y_l, z_l) = TMEM lane
+    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+    const int sw = r & 7;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int s = i % S, n = i / S;
+      tc::mbar_wait(&full[s], n & 1);
+      const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
+      float v[32];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
+        v[4 * c] = q.x;
+        v[4 * c + 1] = q.y;
+        v[4 * c + 2] = q.z;
+        v[4 * c + 3] = q.w;
+      }
+      if constexpr (GRAD) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
+          v[4 * c] = conv<MODE, ACT>(v[4 * c], q.x);
+          v[4 * c + 1] = conv<MODE, ACT>(v[4 * c + 1], q.y);
+          v[4 * c + 2] = conv<MODE, ACT>(v[4 * c + 2], q.z);
+          v[4 * c + 3] = conv<MODE, ACT>(v[4 * c + 3], q.w);
+        }
+      }
+      tc::mbar_arrive(&empty[s]);
+      float h[32], l[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float x = GRAD ? v[k] : conv<MODE, ACT>(v[k], 0.f);
+        tc::split_hl(x, h[k], l[k]);
+      }
+      const int b = i & 1;
+      tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
+      tc::fence_after();
+      tc::tmem_st32(tmem + cAT + 64 * b + lane_off, h);
+      tc::tmem_st32(tmem + cAT + 64 * b + 32 + lane_off, l);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&at_full[b]);
+    }
+  } else if (warp < kConv + kTrans) {
+    // ======================= transposers / epilogue =======================
+    const int q = warp - kConv;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+    float* scr = reinterpret_cast<float*>(smem + L.off_scr + q * kScratchWarp);  // [part][yy][kt][17]
+    float* stash = reinterpret_cast<float*>(smem + L.off_stash);                  // [part][kz][kt][9]
+    const int yy = lane >> 4, lo16 = lane & 15;
+    int chunk = 0, slab_i = 0;
+    for (int G = 0; G < n_groups; ++G) {
+      const int gr = G % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
+      const int b = G & 1;
+      // ---- D1 -> A_Z (within-warp 16x16 transposes, re and im)
+      tc::mbar_wait(&d1_full[b], (G >> 1) & 1);
+      tc::fence_after();
+      uint32_t u[32];
+      tc::tmem_ld32_nowait(tmem + cD1 + 32 * b + lane_off, u);
+      tc::tmem_ld_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&d1_empty[b]);
+#pragma unroll
+      for (int kt = 0; kt < 16; ++kt) {
+        scr[((0 * 2 + yy) * 16 + kt) * 17 + lo16] = __uint_as_float(u[kt]);
+        scr[((1 * 2 + yy) * 16 + kt) * 17 + lo16] = __uint_as_float(u[16 + kt]);
+      }
+      __syncwarp();
+      float h[32], l[32];
+#pragma unroll
+      for (int z = 0; z < 16; ++z) {
+        tc::split_rn(scr[((0 * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
+        tc::split_rn(scr[((1 * 2 + yy) * 16 + lo16) * 17 + z], h[16 + z], l[16 + z]);
+      }
+      __syncwarp();
+      tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1);
+      tc::fence_after();
+      tc::tmem_st32(tmem + cAZ + 64 * b + lane_off, h);
+      tc::tmem_st32(tmem + cAZ + 64 * b + 32 + lane_off, l);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&az_full[b]);
+      if (zb != L.nzb - 1) continue;
+      // ---- chunk end: D2 -> stash -> A_Y (two tiles of (kz, kt) rows)
+      const int cb = chunk & 1;
+      tc::mbar_wait(&d2_full[cb], (chunk >> 1) & 1);
+      tc::fence_after();
+      tc::tmem_ld32_nowait(tmem + cD2 + 32 * cb + lane_off, u);
+      tc::tmem_ld_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&d2_empty[cb]);
+      {
+        const int yl = 2 * q + yy, kt = lo16;  // D2 row (y_l, kt)
+#pragma unroll
+        for (int kz = 0; kz < 16; ++kz) {
+          stash[((0 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u[kz]);
+          stash[((1 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u[16 + kz]);
+        }
+      }
+      tc::named_sync(1, kTrans * 32);
+      float ah[2][16], al[2][16];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int kz = 8 * hh + 2 * q + yy, kt = lo16;  // A_Y row (kz_l, kt) of tile hh
+#pragma unroll
+        for (int y = 0; y < 8; ++y) {
+          tc::split_rn(stash[((0 * 16 + kz) * 16 + kt) * 9 + y], ah[hh][y], al[hh][y]);
+          tc::split_rn(stash[((1 * 16 + kz) * 16 + kt) * 9 + y], ah[hh][8 + y], al[hh][8 + y]);
+        }
+      }
+      tc::named_sync(1, kTrans * 32);
+      tc::mbar_wait(&ay_empty, (chunk & 1) ^ 1);
+      tc::fence_after();
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        tc::tmem_st16(tmem + cAY + 32 * hh + lane_off, ah[hh]);
+        tc::tmem_st16(tmem + cAY + 32 * hh + 16 + lane_off, al[hh]);
+      }
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&ay_full);
+      ++chunk;
+      if (yc != L.nyc - 1) continue;
+      // ---- slab end: D3 -> XK exchange layout
+      const int slab = (int)blockIdx.x + (G / groups_per_slab) * (int)gridDim.x;
+      const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
+      tc::mbar_wait(&d3_full, slab_i & 1);
+      tc::fence_after();
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        tc::tmem_ld32_nowait(tmem + cD3 + 32 * hh + lane_off, u);
+        tc::tmem_ld_wait();
+        const int kz = 8 * hh + 2 * q + yy, kt = lo16;
+        if (kz < g.rz && kt < g.rt) {
+#pragma unroll
+          for (int ky = 0; ky < 16; ++ky)
+            if (ky < g.ry)
+              out[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt] =
+                  make_float2(scale * __uint_as_float(u[ky]), scale * __uint_as_float(u[16 + ky]));
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&d3_empty);
+      ++slab_i;
+    }
+  } else if (warp == kConv + kTrans + 1) {
+    // ======================= MMA issuer: stage T =======================
+    if (lane == 0) {
+      const uint32_t id = tc::idesc_tf32(128, 32);
+      const uint32_t sbt = tc::smem_u32(bt), plt = 4 * L.sbo_t;
+      int i = 0;
+      for (int G = 0; G < n_groups; ++G) {
+        const int b = G & 1;
+        tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1);
+        for (int tb = 0; tb < L.ntb; ++tb, ++i) {
+          const int ab = i & 1;
+          tc::mbar_wait(&at_full[ab], (i >> 1) & 1);
+          tc::fence_after();
+          const uint32_t a = tmem + cAT + 64 * ab, d = tmem + cD1 + 32 * b;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t kb = (uint32_t)(tb * 4 + s) * 256;
+            const uint64_t bh = tc::desc(sbt + kb, 128, L.sbo_t), bl = tc::desc(sbt + plt + kb, 128, L.sbo_t);
+            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (tb | s) ? 1u : 0u);
+            tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
+            tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+          }
+          tc::commit(&at_empty[ab]);
+        }
+        tc::commit(&d1_full[b]);
+      }
+    }
+  } else {
+    // ======================= MMA issuer: stages Z and Y =======================
+    if (lane == 0) {
+      const uint32_t id = tc::idesc_tf32(128, 32);
+      const uint32_t sbz = tc::smem_u32(bz), plz = 4 * L.sbo_z;
+      const uint32_t sby = tc::smem_u32(by), ply = 4 * L.sbo_y;
+      int chunk = 0, slab_i = 0;
+      for (int G = 0; G < n_groups; ++G) {
+        const int gr = G % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
+        const int b = G & 1, cb = chunk & 1;
+        tc::mbar_wait(&az_full[b], (G >> 1) & 1);
+        if (zb == 0) tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1);
+        tc::fence_after();
+        {
+          const uint32_t a = tmem + cAZ + 64 * b, d = tmem + cD2 + 32 * cb;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t kb = (uint32_t)(zb * 4 + s) * 256;
+            const uint64_t bh = tc::desc(sbz + kb, 128, L.sbo_z), bl = tc::desc(sbz + plz + kb, 128, L.sbo_z);
+            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (zb | s) ? 1u : 0u);
+            tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
+            tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+          }
+        }
+        tc::commit(&az_empty[b]);
+        if (zb != L.nzb - 1) continue;
+        tc::commit(&d2_full[cb]);
+        // ---- stage Y for this chunk
+        tc::mbar_wait(&ay_full, chunk & 1);
+        if (yc == 0) tc::mbar_wait(&d3_empty, (slab_i & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t a = tmem + cAY + 32 * hh, d = tmem + cD3 + 32 * hh;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const uint32_t kb = (uint32_t)(yc * 2 + s) * 256;
+            const uint64_t bh = tc::desc(sby + kb, 128, L.sbo_y), bl = tc::desc(sby + ply + kb, 128, L.sbo_y);
+            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (yc | s) ? 1u : 0u);
+            tc::mma_tf32_ts(d, a + 16 + 8 * s, bh, id, 1u);
+            tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+          }
+        }
+        tc::commit(&ay_empty);
+        ++chunk;
+        if (yc == L.nyc - 1) {
+          tc::commit(&d3_full);
+          ++slab_i;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+namespace {
+
+int sm_count2() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int smem_optin() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (n <= 0) n = 227 * 1024;
+    n -= 2048 + 1024;  // static shared memory of the kernel, alignment slack
+  }
+  return n;
+}
+
+// 4-D map over (t, z, y, slab) of a (slabs, Ny, Nz, Nt) fp32 tensor, box
+// (32, 16, 8, 1), 128-byte swizzle, out-of-bounds zero fill.
+bool make_map(CUtensorMap* m, const void* base, int ny, int nz, int nt, int slabs) {
+  cuuint64_t dims[4] = {(cuuint64_t)nt, (cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)slabs};
+  cuuint64_t strides[3] = {(cuuint64_t)nt * 4, (cuuint64_t)nz * nt * 4, (cuuint64_t)ny * nz * nt * 4};
+  cuuint32_t box[4] = {32, 16, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
+                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE, int ACT>
+int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, void* out, cudaStream_t st) {
+  const int cap = smem_optin();
+  const Lay L = make_lay(g.ny, g.nz, g.nt, MODE == DFNO_SRC_GRAD ? 2 : 1, cap);
+  if (L.stages < 2) return DFNO_ERR_UNSUPPORTED;
+  const int slabs = g.batch * g.c * x_local(g);
+  CUtensorMap ms, mp;
+  if (!make_map(&ms, src, g.ny, g.nz, g.nt, slabs)) return DFNO_ERR_UNSUPPORTED;
+  if (MODE == DFNO_SRC_GRAD) {
+    if (!make_map(&mp, pre, g.ny, g.nz, g.nt, slabs)) return DFNO_ERR_UNSUPPORTED;
+  } else {
+    mp = ms;
+  }
+  auto kern = k_yzt_fwd_tc2<MODE, ACT>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  const int grid = sm_count2() < slabs ? sm_count2() : slabs;
+  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+template <int MODE>
+int launch2_act(const dfno_geom& g, const void* src, const void* pre, double scale, void* out, cudaStream_t st) {
+  switch (g.act) {
+    case DFNO_ACT_GELU: return launch2<MODE, DFNO_ACT_GELU>(g, src, pre, scale, out, st);
+    case DFNO_ACT_RELU: return launch2<MODE, DFNO_ACT_RELU>(g, src, pre, scale, out, st);
+    default: return launch2<MODE, DFNO_ACT_IDENTITY>(g, src, pre, scale, out, st);
+  }
+}
+
+}  // namespace
+
+int yzt_fwd_tc2(const dfno_geom& g, const void* src, const void* pre, int mode, double scale, void* out,
+                cudaStream_t st) {
+  if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;
+  if (g.nt % 4 != 0 || ((uintptr_t)src & 15) || (pre && ((uintptr_t)pre & 15))) return DFNO_ERR_UNSUPPORTED;
+  switch (mode) {
+    case DFNO_SRC_ACT: return launch2_act<DFNO_SRC_ACT>(g, src, pre, scale, out, st);
+    case DFNO_SRC_GRAD: return launch2_act<DFNO_SRC_GRAD>(g, src, pre, scale, out, st);
+    default: return launch2<DFNO_SRC_RAW, DFNO_ACT_IDENTITY>(g, src, pre, scale, out, st);
+  }
+}
+
+}  // namespace dfno

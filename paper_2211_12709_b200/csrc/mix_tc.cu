@@ -40,13 +40,16 @@ __device__ __forceinline__ int mb_off(int r, int k) {
 }
 }  // namespace
 
-template <int CM>
-__global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, int nb, int cin, int cout,
+// CM: channel bucket (>= cin, cout); EXACT: cin == cout == CM (no channel
+// masks); ACT: activation code (compile time: no per-element branches).
+template <int CM, bool EXACT, int ACT>
+__global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, int nb, int cin_rt, int cout_rt,
                                                               const float* __restrict__ gout,
                                                               const float* __restrict__ pre,
-                                                              const float* __restrict__ src, int src_act, int act,
+                                                              const float* __restrict__ src, int src_act,
                                                               const float* __restrict__ w, float* __restrict__ gin,
                                                               float* __restrict__ partials) {
+  const int cin = EXACT ? CM : cin_rt, cout = EXACT ? CM : cout_rt;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -94,36 +97,51 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     if (prev_out >= 0) {
 #pragma unroll
       for (int i = 0; i < CM; ++i)
-        if (i < cin) __stcs(gin + prev_out + (long long)i * npts, __uint_as_float(r[i]));
+        if (EXACT || i < cin) __stcs(gin + prev_out + (long long)i * npts, __uint_as_float(r[i]));
     }
   };
 
+  // register double buffer: tile i + 1 is loaded while tile i is converted
+  float gv[CM], pv[CM], sv[CM];
+  auto load = [&](long long tile) {
+    const long long bb = tile / tiles_per_b;
+    const long long p = (tile - bb * tiles_per_b) * kMbThreads + tid;
+    const bool valid = tile < ntiles && p < npts;
+    const float* g0 = gout + (bb * cout) * npts + p;
+    const float* p0 = pre + (bb * cout) * npts + p;
+    const float* s0 = src + (bb * cin) * npts + p;
+#pragma unroll
+    for (int o = 0; o < CM; ++o) {
+      const bool ok = valid && (EXACT || o < cout);
+      gv[o] = ok ? __ldcs(g0) : 0.f;
+      pv[o] = ok ? __ldcs(p0) : 0.f;
+      g0 += npts;
+      p0 += npts;
+    }
+#pragma unroll
+    for (int i = 0; i < CM; ++i) {
+      sv[i] = (valid && (EXACT || i < cin)) ? __ldg(s0) : 0.f;
+      s0 += npts;
+    }
+  };
+  load(blockIdx.x);
 #pragma unroll 1
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const long long bb = tile / tiles_per_b;
     const long long p = (tile - bb * tiles_per_b) * kMbThreads + tid;
     const bool valid = p < npts;
-    float gv[CM], pv[CM], sv[CM];
-    {
-      const float* g0 = gout + bb * cout * npts + p;
-      const float* p0 = pre + bb * cout * npts + p;
-      const float* s0 = src + bb * cin * npts + p;
-#pragma unroll
-      for (int o = 0; o < CM; ++o) {
-        const bool ok = valid && o < cout;
-        gv[o] = ok ? __ldcs(g0 + (long long)o * npts) : 0.f;
-        pv[o] = ok ? __ldcs(p0 + (long long)o * npts) : 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < CM; ++i) sv[i] = (valid && i < cin) ? __ldg(s0 + (long long)i * npts) : 0.f;
-    }
+    float gp[CM], a[CM];
     // gp = g * act'(pre) ; a = act(src) or src  (zero for padding / invalid points)
 #pragma unroll
-    for (int o = 0; o < CM; ++o) gv[o] *= act_deriv<float>(act, pv[o]);
+    for (int o = 0; o < CM; ++o) gp[o] = gv[o] * act_deriv<float>(ACT, pv[o]);
     if (src_act) {
 #pragma unroll
-      for (int i = 0; i < CM; ++i) sv[i] = act_apply<float>(act, sv[i]);
+      for (int i = 0; i < CM; ++i) a[i] = act_apply<float>(ACT, sv[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < CM; ++i) a[i] = sv[i];
     }
+    load(tile + gridDim.x);
     if (it > 0) {  // MMAs of the previous tile done: its operands are free, D1 holds its input grad
       tc::mbar_wait(&bar, (it - 1) & 1);
       tc::fence_after();
@@ -133,7 +151,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       float h[32], l[32];
 #pragma unroll
       for (int o = 0; o < 32; ++o) {
-        if (o < CM) tc::split_rn(gv[o], h[o], l[o]);
+        if (o < CM) tc::split_rn(gp[o], h[o], l[o]);
         else h[o] = l[o] = 0.f;
       }
       tc::tmem_st32(a1h + lane_off, h);
@@ -141,18 +159,18 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     }
 #pragma unroll
     for (int i = 0; i < CM; ++i) {
-      if (i < cin) {
+      if (EXACT || i < cin) {
         float h, l;
-        tc::split_rn(sv[i], h, l);
+        tc::split_rn(a[i], h, l);
         *reinterpret_cast<float*>(a2 + mb_off(i, tid)) = h;
         *reinterpret_cast<float*>(a2 + mb_off(32 + i, tid)) = l;
       }
     }
 #pragma unroll
     for (int o = 0; o < CM; ++o) {
-      if (o < cout) {
+      if (EXACT || o < cout) {
         float h, l;
-        tc::split_rn(gv[o], h, l);
+        tc::split_rn(gp[o], h, l);
         *reinterpret_cast<float*>(b2 + mb_off(o, tid)) = h;
         *reinterpret_cast<float*>(b2 + mb_off(32 + o, tid)) = l;
       }
@@ -217,19 +235,36 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   if (warp == 0) tc::tmem_dealloc<kMbTmemCols>(tmem);
 }
 
-template <int CM>
-static int launch_mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
-                             const void* src, int src_act, int act, const void* w, void* gin, void* partials,
-                             int blocks, cudaStream_t st) {
+template <int CM, bool EXACT, int ACT>
+static int launch_mix_bwd_tc3(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                              const void* src, int src_act, const void* w, void* gin, void* partials, int blocks,
+                              cudaStream_t st) {
   const int smem = 2 * kMbOpBytes + 2 * 4 * 1024;
-  auto kern = k_mix_bwd_tc<CM>;
+  auto kern = k_mix_bwd_tc<CM, EXACT, ACT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   kern<<<blocks, kMbThreads, smem, st>>>(npts, nb, cin, cout, (const float*)gout, (const float*)pre,
-                                         (const float*)src, src_act, act, (const float*)w, (float*)gin,
+                                         (const float*)src, src_act, (const float*)w, (float*)gin,
                                          (float*)partials);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
+}
+
+template <int CM, bool EXACT>
+static int launch_mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
+                             const void* src, int src_act, int act, const void* w, void* gin, void* partials,
+                             int blocks, cudaStream_t st) {
+  switch (act) {
+    case DFNO_ACT_GELU:
+      return launch_mix_bwd_tc3<CM, EXACT, DFNO_ACT_GELU>(npts, nb, cin, cout, gout, pre, src, src_act, w, gin,
+                                                          partials, blocks, st);
+    case DFNO_ACT_RELU:
+      return launch_mix_bwd_tc3<CM, EXACT, DFNO_ACT_RELU>(npts, nb, cin, cout, gout, pre, src, src_act, w, gin,
+                                                          partials, blocks, st);
+    default:
+      return launch_mix_bwd_tc3<CM, EXACT, DFNO_ACT_IDENTITY>(npts, nb, cin, cout, gout, pre, src, src_act, w, gin,
+                                                              partials, blocks, st);
+  }
 }
 
 // fp32, cin and cout <= 32; returns DFNO_ERR_UNSUPPORTED otherwise.
@@ -237,12 +272,14 @@ int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, cons
                int src_act, int act, const void* w, void* gin, void* partials, int blocks, cudaStream_t st) {
   const int m = cin > cout ? cin : cout;
   if (m > 32 || blocks < 1) return DFNO_ERR_UNSUPPORTED;
-  if (m <= 8) return launch_mix_bwd_tc<8>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
-  if (m <= 16)
-    return launch_mix_bwd_tc<16>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
-  if (m <= 24)
-    return launch_mix_bwd_tc<24>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
-  return launch_mix_bwd_tc<32>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st);
+#define DFNO_MB(CM, EX) \
+  return launch_mix_bwd_tc<CM, EX>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, blocks, st)
+  if (cin == 20 && cout == 20) DFNO_MB(20, true);
+  if (m <= 8) DFNO_MB(8, false);
+  if (m <= 16) DFNO_MB(16, false);
+  if (m <= 24) DFNO_MB(24, false);
+  DFNO_MB(32, false);
+#undef DFNO_MB
 }
 
 }  // namespace dfno
