@@ -43,21 +43,29 @@ namespace dfno {
 
 namespace {
 
-constexpr int kConv = 4, kTrans = 4;
-constexpr int kWarps = kConv + kTrans + 3;  // + TMA producer, MMA-T issuer, MMA-ZY issuer
+// warp roles
+constexpr int kConvW = 8;                 // converters: two sets of 4 (tile parity), one warp per TMEM quarter
+constexpr int kTepiW0 = 8;                // warps 8-11: D1 -> A_Z
+constexpr int kZepiW0 = 12;               // warps 12-15: D2 -> A_Y, D3 -> output
+constexpr int kTmaW = 16;                 // TMA producer
+constexpr int kIssT0 = 17, kIssT1 = 18;   // stage-T issuers (group parity when one t block per group)
+constexpr int kIssZ = 19, kIssY = 20;     // stage-Z / stage-Y issuers
+constexpr int kWarps = 21;
 constexpr int kThreads2 = kWarps * 32;
-constexpr int kTileBytes = 128 * 32 * 4;     // 128 rows x 32 t fp32
+constexpr int kTileBytes = 128 * 32 * 4;            // 128 rows x 32 t fp32
 constexpr int kScratchWarp = 2 * 2 * 16 * 17 * 4;   // [part][yy][kt][z (+1)]
 constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
+constexpr int kAYPlane = 16 * 512;                  // 128 rows x K 16, SBO 512 (one hi or lo plane of one tile)
+constexpr int kAYBytes = 4 * kAYPlane;              // 2 tiles x (hi, lo)
 
-// TMEM column map
-constexpr uint32_t cAT = 0, cD1 = 128, cAZ = 192, cD2 = 320, cAY = 384, cD3 = 448;
+// TMEM column map (512): A_T 2x64 | D1 2x32 | A_Z 2x64 | D2 2x64 (hi.hi+lo.hi | hi.lo) | D3 2 tiles x 32
+constexpr uint32_t cAT = 0, cD1 = 128, cAZ = 192, cD2 = 320, cD3 = 448;
 
 struct Lay {
   int nyc, nzb, ntb;            // y chunks (8), z blocks (16), t blocks (32)
   int kt_tot, kz_tot, ky_tot;   // K extents of the twiddle operands
   int sbo_t, sbo_z, sbo_y;
-  int off_ring, off_bt, off_bz, off_by, off_scr, off_stash, total;
+  int off_ring, off_bt, off_bz, off_by, off_scr, off_stash, off_ay, total;
   int stages, srcs;             // ring depth, tiles per stage (1 or 2)
 };
 
@@ -77,15 +85,16 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.off_bt = o; o += 2 * 4 * L.sbo_t;   // hi, lo planes of 32 rows
   L.off_bz = o; o += 2 * 4 * L.sbo_z;
   L.off_by = o; o += 2 * 4 * L.sbo_y;
-  L.off_scr = o; o += kTrans * kScratchWarp;
+  L.off_scr = o; o += 4 * kScratchWarp;
   L.off_stash = o; o += kStashBytes;
   o = (o + 1023) & ~1023;
+  L.off_ay = o; o += kAYBytes;
   L.off_ring = o;
   const int stage = srcs * kTileBytes;
   int s = (smem_cap - o) / stage;
-  if (s > 4) s = 4;
+  s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);  // even: ring stage s always holds tiles of parity s & 1
   L.stages = s;
-  L.total = o + (s > 0 ? s : 0) * stage;
+  L.total = o + s * stage;
   return L;
 }
 
@@ -115,6 +124,18 @@ __device__ __forceinline__ float conv(float v, float p) {
   return v;
 }
 
+// (y chunk, z block) of group G, walked incrementally
+struct GroupIdx {
+  int yc = 0, zb = 0, slab_g = 0;
+  __device__ void next(const Lay& L) {
+    if (++zb < L.nzb) return;
+    zb = 0;
+    if (++yc < L.nyc) return;
+    yc = 0;
+    ++slab_g;
+  }
+};
+
 }  // namespace
 
 template <int MODE, int ACT>
@@ -135,8 +156,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
   unsigned char* bt = smem + L.off_bt;
   unsigned char* bz = smem + L.off_bz;
   unsigned char* by = smem + L.off_by;
+  unsigned char* ay = smem + L.off_ay;
 
-  // ---- twiddle operands (hi / lo planes, K-major, 32 rows) ---------------
+  // ---- twiddle operands (hi / lo planes, K-major, 32 rows each) -----------
   {
     const int pl = 4 * L.sbo_t;  // t: rows 0-15 cos(kt), 16-31 -sin(kt); K = t
     for (int e = tid; e < 32 * L.kt_tot; e += blockDim.x) {
@@ -145,18 +167,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
       cs(n & 15, t, Nt, g.mt, g.rt, c, s);
       put_split(bt, pl, kmaj32(n, t, L.sbo_t), n < 16 ? c : -s);
     }
-  }
-  {
     // z / y: realified complex e^{-i}: K = (block, part, index); rows 0-15 out
-    // re (C on re, S on im), rows 16-31 out im (-S on re, C on im)
+    // re (C on re, S on im), rows 16-31 out im (-S on re, C on im).  The lo
+    // plane sits 32 rows below the hi plane, so one N = 64 descriptor covers
+    // [hi | lo] (stage Z stacks them in a single MMA).
     const int plz = 4 * L.sbo_z;
     for (int e = tid; e < 32 * L.kz_tot; e += blockDim.x) {
       const int n = e / L.kz_tot, k = e % L.kz_tot;
       const int z = (k / 32) * 16 + (k & 15), part = (k >> 4) & 1;
       double c, s;
       cs(n & 15, z, Nz, g.mz, g.rz, c, s);
-      const double v = (n < 16) ? (part ? s : c) : (part ? c : -s);
-      put_split(bz, plz, kmaj32(n, k, L.sbo_z), v);
+      put_split(bz, plz, kmaj32(n, k, L.sbo_z), (n < 16) ? (part ? s : c) : (part ? c : -s));
     }
     const int ply = 4 * L.sbo_y;
     for (int e = tid; e < 32 * L.ky_tot; e += blockDim.x) {
@@ -164,30 +185,29 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const int y = (k / 16) * 8 + (k & 7), part = (k >> 3) & 1;
       double c, s;
       cs(n & 15, y, Ny, g.my, g.ry, c, s);
-      const double v = (n < 16) ? (part ? s : c) : (part ? c : -s);
-      put_split(by, ply, kmaj32(n, k, L.sbo_y), v);
+      put_split(by, ply, kmaj32(n, k, L.sbo_y), (n < 16) ? (part ? s : c) : (part ? c : -s));
     }
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int s = 0; s < 4; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], kConv * 32);
+      tc::mbar_init(&empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&at_full[b], kConv * 32);
+      tc::mbar_init(&at_full[b], 128);
       tc::mbar_init(&at_empty[b], 1);
       tc::mbar_init(&d1_full[b], 1);
-      tc::mbar_init(&d1_empty[b], kTrans * 32);
-      tc::mbar_init(&az_full[b], kTrans * 32);
+      tc::mbar_init(&d1_empty[b], 128);
+      tc::mbar_init(&az_full[b], 128);
       tc::mbar_init(&az_empty[b], 1);
       tc::mbar_init(&d2_full[b], 1);
-      tc::mbar_init(&d2_empty[b], kTrans * 32);
+      tc::mbar_init(&d2_empty[b], 128);
     }
-    tc::mbar_init(&ay_full, kTrans * 32);
+    tc::mbar_init(&ay_full, 128);
     tc::mbar_init(&ay_empty, 1);
     tc::mbar_init(&d3_full, 1);
-    tc::mbar_init(&d3_empty, kTrans * 32);
+    tc::mbar_init(&d3_empty, 128);
     tc::mbar_fence_init();
   }
   tc::fence_proxy_async();
@@ -201,85 +221,54 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int groups_per_slab = L.nyc * L.nzb;
   const int n_groups = my_slabs * groups_per_slab;
   const int n_tiles = n_groups * L.ntb;
+  const int n_chunks = my_slabs * L.nyc;
   const int S = L.stages;
+  const bool two_t = (L.ntb == 1);
+  const uint32_t quarter_off = (uint32_t)(32 * (warp & 3)) << 16;
 
-  if (warp == kConv + kTrans) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      tc::tma_prefetch_desc(&tm_src);
-      if (GRAD) tc::tma_prefetch_desc(&tm_pre);
-      for (int i = 0; i < n_tiles; ++i) {
-        const int s = i % S, n = i / S;
-        const int tb = i % L.ntb, gi = i / L.ntb;
-        const int slab = (int)blockIdx.x + (gi / groups_per_slab) * (int)gridDim.x;
-        const int gr = gi % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
-        tc::mbar_wait(&empty[s], (n & 1) ^ 1);
-        tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
-        unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
-        tc::tma_load_4d(dst, &tm_src, tb * 32, zb * 16, yc * 8, slab, &full[s]);
-        if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, zb * 16, yc * 8, slab, &full[s]);
-      }
-    }
-  } else if (warp < kConv) {
+  if (warp < kConvW) {
     // ======================= converters =======================
-    const int r = tid;  // tile row = (y_l, z_l) = TMEM lane
-    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+    const int set = warp >> 2, r = 32 * (warp & 3) + lane;  // tile row (y_l, z_l) = TMEM lane
     const int sw = r & 7;
-    for (int i = 0; i < n_tiles; ++i) {
+    for (int i = set; i < n_tiles; i += 2) {
       const int s = i % S, n = i / S;
       tc::mbar_wait(&full[s], n & 1);
       const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
-      float v[32];
+      const int b = i & 1;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
-        v[4 * c] = q.x;
-        v[4 * c + 1] = q.y;
-        v[4 * c + 2] = q.z;
-        v[4 * c + 3] = q.w;
-      }
-      if constexpr (GRAD) {
+      for (int half = 0; half < 2; ++half) {
+        float h[16], l[16];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 q = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
-          v[4 * c] = conv<MODE, ACT>(v[4 * c], q.x);
-          v[4 * c + 1] = conv<MODE, ACT>(v[4 * c + 1], q.y);
-          v[4 * c + 2] = conv<MODE, ACT>(v[4 * c + 2], q.z);
-          v[4 * c + 3] = conv<MODE, ACT>(v[4 * c + 3], q.w);
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int c = 4 * half + c4;
+          const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
+          float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (GRAD) p = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
+          tc::split_hl(conv<MODE, ACT>(q.x, p.x), h[4 * c4], l[4 * c4]);
+          tc::split_hl(conv<MODE, ACT>(q.y, p.y), h[4 * c4 + 1], l[4 * c4 + 1]);
+          tc::split_hl(conv<MODE, ACT>(q.z, p.z), h[4 * c4 + 2], l[4 * c4 + 2]);
+          tc::split_hl(conv<MODE, ACT>(q.w, p.w), h[4 * c4 + 3], l[4 * c4 + 3]);
         }
+        if (half == 0) tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
+        tc::tmem_st16(tmem + cAT + 64 * b + 16 * half + quarter_off, h);
+        tc::tmem_st16(tmem + cAT + 64 * b + 32 + 16 * half + quarter_off, l);
       }
       tc::mbar_arrive(&empty[s]);
-      float h[32], l[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float x = GRAD ? v[k] : conv<MODE, ACT>(v[k], 0.f);
-        tc::split_hl(x, h[k], l[k]);
-      }
-      const int b = i & 1;
-      tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
-      tc::fence_after();
-      tc::tmem_st32(tmem + cAT + 64 * b + lane_off, h);
-      tc::tmem_st32(tmem + cAT + 64 * b + 32 + lane_off, l);
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&at_full[b]);
     }
-  } else if (warp < kConv + kTrans) {
-    // ======================= transposers / epilogue =======================
-    const int q = warp - kConv;
-    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
+  } else if (warp < kZepiW0) {
+    // ======================= T epilogue: D1 -> A_Z =======================
+    const int q = warp - kTepiW0;
     float* scr = reinterpret_cast<float*>(smem + L.off_scr + q * kScratchWarp);  // [part][yy][kt][17]
-    float* stash = reinterpret_cast<float*>(smem + L.off_stash);                  // [part][kz][kt][9]
     const int yy = lane >> 4, lo16 = lane & 15;
-    int chunk = 0, slab_i = 0;
     for (int G = 0; G < n_groups; ++G) {
-      const int gr = G % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
       const int b = G & 1;
-      // ---- D1 -> A_Z (within-warp 16x16 transposes, re and im)
       tc::mbar_wait(&d1_full[b], (G >> 1) & 1);
       tc::fence_after();
       uint32_t u[32];
-      tc::tmem_ld32_nowait(tmem + cD1 + 32 * b + lane_off, u);
+      tc::tmem_ld32_nowait(tmem + cD1 + 32 * b + quarter_off, u);
       tc::tmem_ld_wait();
       tc::fence_before();
       tc::mbar_arrive(&d1_empty[b]);
@@ -292,66 +281,81 @@ __global__ void __launch_bounds__(kThreads2, 1)
       float h[32], l[32];
 #pragma unroll
       for (int z = 0; z < 16; ++z) {
-        tc::split_rn(scr[((0 * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
-        tc::split_rn(scr[((1 * 2 + yy) * 16 + lo16) * 17 + z], h[16 + z], l[16 + z]);
+        tc::split_hl(scr[((0 * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
+        tc::split_hl(scr[((1 * 2 + yy) * 16 + lo16) * 17 + z], h[16 + z], l[16 + z]);
       }
       __syncwarp();
       tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1);
       tc::fence_after();
-      tc::tmem_st32(tmem + cAZ + 64 * b + lane_off, h);
-      tc::tmem_st32(tmem + cAZ + 64 * b + 32 + lane_off, l);
+      tc::tmem_st32(tmem + cAZ + 64 * b + quarter_off, h);
+      tc::tmem_st32(tmem + cAZ + 64 * b + 32 + quarter_off, l);
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&az_full[b]);
-      if (zb != L.nzb - 1) continue;
-      // ---- chunk end: D2 -> stash -> A_Y (two tiles of (kz, kt) rows)
-      const int cb = chunk & 1;
-      tc::mbar_wait(&d2_full[cb], (chunk >> 1) & 1);
+    }
+  } else if (warp < kTmaW) {
+    // ======================= Z epilogue: D2 -> A_Y (smem), D3 -> XK =======================
+    const int q = warp - kZepiW0;
+    float* stash = reinterpret_cast<float*>(smem + L.off_stash);  // [part][kz][kt][9]
+    const int yy = lane >> 4, lo16 = lane & 15;
+    const int row = 32 * q + lane;  // A_Y / D3 row (kz_l, kt)
+    int slab_i = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int yc = c % L.nyc, cb = c & 1;
+      tc::mbar_wait(&d2_full[cb], (c >> 1) & 1);
       tc::fence_after();
-      tc::tmem_ld32_nowait(tmem + cD2 + 32 * cb + lane_off, u);
-      tc::tmem_ld_wait();
+      uint32_t u0[32];
+      {
+        uint32_t u1[32];
+        tc::tmem_ld32_nowait(tmem + cD2 + 64 * cb + quarter_off, u0);
+        tc::tmem_ld32_nowait(tmem + cD2 + 64 * cb + 32 + quarter_off, u1);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) u0[j] = __float_as_uint(__uint_as_float(u0[j]) + __uint_as_float(u1[j]));
+      }
       tc::fence_before();
       tc::mbar_arrive(&d2_empty[cb]);
       {
-        const int yl = 2 * q + yy, kt = lo16;  // D2 row (y_l, kt)
+        const int yl = 2 * q + yy, kt = lo16;  // D2 row (y_l, kt): (hi.hi + lo.hi) + hi.lo
 #pragma unroll
         for (int kz = 0; kz < 16; ++kz) {
-          stash[((0 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u[kz]);
-          stash[((1 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u[16 + kz]);
+          stash[((0 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u0[kz]);
+          stash[((1 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u0[16 + kz]);
         }
       }
-      tc::named_sync(1, kTrans * 32);
-      float ah[2][16], al[2][16];
-#pragma unroll
+      tc::named_sync(1, 128);
+      tc::mbar_wait(&ay_empty, (c & 1) ^ 1);
+#pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
-        const int kz = 8 * hh + 2 * q + yy, kt = lo16;  // A_Y row (kz_l, kt) of tile hh
+        // A_Y tile hh row (kz_l, kt), K = (re y0..7, im y0..7), hi / lo planes,
+        // K-major (LBO 128, SBO 512)
+        const int kz = 8 * hh + 2 * q + yy, kt = lo16;
+        float ah[16], al[16];
 #pragma unroll
         for (int y = 0; y < 8; ++y) {
-          tc::split_rn(stash[((0 * 16 + kz) * 16 + kt) * 9 + y], ah[hh][y], al[hh][y]);
-          tc::split_rn(stash[((1 * 16 + kz) * 16 + kt) * 9 + y], ah[hh][8 + y], al[hh][8 + y]);
+          tc::split_rn(stash[((0 * 16 + kz) * 16 + kt) * 9 + y], ah[y], al[y]);
+          tc::split_rn(stash[((1 * 16 + kz) * 16 + kt) * 9 + y], ah[8 + y], al[8 + y]);
+        }
+        unsigned char* th = ay + (2 * hh) * kAYPlane + (row >> 3) * 512 + (row & 7) * 16;
+        unsigned char* tl = th + kAYPlane;
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          *reinterpret_cast<float4*>(th + k4 * 128) = make_float4(ah[4 * k4], ah[4 * k4 + 1], ah[4 * k4 + 2], ah[4 * k4 + 3]);
+          *reinterpret_cast<float4*>(tl + k4 * 128) = make_float4(al[4 * k4], al[4 * k4 + 1], al[4 * k4 + 2], al[4 * k4 + 3]);
         }
       }
-      tc::named_sync(1, kTrans * 32);
-      tc::mbar_wait(&ay_empty, (chunk & 1) ^ 1);
-      tc::fence_after();
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        tc::tmem_st16(tmem + cAY + 32 * hh + lane_off, ah[hh]);
-        tc::tmem_st16(tmem + cAY + 32 * hh + 16 + lane_off, al[hh]);
-      }
-      tc::tmem_st_wait();
-      tc::fence_before();
+      tc::named_sync(1, 128);  // stash consumed before the next chunk overwrites it
+      tc::fence_proxy_async();
       tc::mbar_arrive(&ay_full);
-      ++chunk;
       if (yc != L.nyc - 1) continue;
       // ---- slab end: D3 -> XK exchange layout
-      const int slab = (int)blockIdx.x + (G / groups_per_slab) * (int)gridDim.x;
+      const int slab = (int)blockIdx.x + slab_i * (int)gridDim.x;
       const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
       tc::mbar_wait(&d3_full, slab_i & 1);
       tc::fence_after();
-#pragma unroll
+#pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
-        tc::tmem_ld32_nowait(tmem + cD3 + 32 * hh + lane_off, u);
+        tc::tmem_ld32_nowait(tmem + cD3 + 32 * hh + quarter_off, u0);
         tc::tmem_ld_wait();
         const int kz = 8 * hh + 2 * q + yy, kt = lo16;
         if (kz < g.rz && kt < g.rt) {
@@ -359,24 +363,45 @@ __global__ void __launch_bounds__(kThreads2, 1)
           for (int ky = 0; ky < 16; ++ky)
             if (ky < g.ry)
               out[xk_row(g, bb, ch, xl, ky) + kz * g.rt + kt] =
-                  make_float2(scale * __uint_as_float(u[ky]), scale * __uint_as_float(u[16 + ky]));
+                  make_float2(scale * __uint_as_float(u0[ky]), scale * __uint_as_float(u0[16 + ky]));
         }
       }
       tc::fence_before();
       tc::mbar_arrive(&d3_empty);
       ++slab_i;
     }
-  } else if (warp == kConv + kTrans + 1) {
-    // ======================= MMA issuer: stage T =======================
+  } else if (warp == kTmaW) {
+    // ======================= TMA producer =======================
     if (lane == 0) {
+      tc::tma_prefetch_desc(&tm_src);
+      if (GRAD) tc::tma_prefetch_desc(&tm_pre);
+      GroupIdx gi;
+      int tb = 0;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int s = i % S, n = i / S;
+        const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
+        tc::mbar_wait(&empty[s], (n & 1) ^ 1);
+        tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
+        unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
+        tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+        if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+        if (++tb == L.ntb) {
+          tb = 0;
+          gi.next(L);
+        }
+      }
+    }
+  } else if (warp == kIssT0 || warp == kIssT1) {
+    // ======================= stage T issuers =======================
+    const int k = warp - kIssT0;
+    if (lane == 0 && (two_t || k == 0)) {
       const uint32_t id = tc::idesc_tf32(128, 32);
       const uint32_t sbt = tc::smem_u32(bt), plt = 4 * L.sbo_t;
-      int i = 0;
-      for (int G = 0; G < n_groups; ++G) {
+      for (int G = two_t ? k : 0; G < n_groups; G += two_t ? 2 : 1) {
         const int b = G & 1;
         tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1);
-        for (int tb = 0; tb < L.ntb; ++tb, ++i) {
-          const int ab = i & 1;
+        for (int tb = 0; tb < L.ntb; ++tb) {
+          const int i = G * L.ntb + tb, ab = i & 1;
           tc::mbar_wait(&at_full[ab], (i >> 1) & 1);
           tc::fence_after();
           const uint32_t a = tmem + cAT + 64 * ab, d = tmem + cD1 + 32 * b;
@@ -393,51 +418,59 @@ __global__ void __launch_bounds__(kThreads2, 1)
         tc::commit(&d1_full[b]);
       }
     }
-  } else {
-    // ======================= MMA issuer: stages Z and Y =======================
+  } else if (warp == kIssZ) {
+    // ======================= stage Z issuer (hi/lo twiddles stacked, N = 64) ==========
     if (lane == 0) {
-      const uint32_t id = tc::idesc_tf32(128, 32);
-      const uint32_t sbz = tc::smem_u32(bz), plz = 4 * L.sbo_z;
-      const uint32_t sby = tc::smem_u32(by), ply = 4 * L.sbo_y;
-      int chunk = 0, slab_i = 0;
+      const uint32_t id64 = tc::idesc_tf32(128, 64), id32 = tc::idesc_tf32(128, 32);
+      const uint32_t sbz = tc::smem_u32(bz);
+      GroupIdx gi;
+      int chunk = 0;
       for (int G = 0; G < n_groups; ++G) {
-        const int gr = G % groups_per_slab, yc = gr / L.nzb, zb = gr % L.nzb;
         const int b = G & 1, cb = chunk & 1;
         tc::mbar_wait(&az_full[b], (G >> 1) & 1);
-        if (zb == 0) tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1);
+        if (gi.zb == 0) tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1);
         tc::fence_after();
-        {
-          const uint32_t a = tmem + cAZ + 64 * b, d = tmem + cD2 + 32 * cb;
+        const uint32_t a = tmem + cAZ + 64 * b, d = tmem + cD2 + 64 * cb;
 #pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const uint32_t kb = (uint32_t)(zb * 4 + s) * 256;
-            const uint64_t bh = tc::desc(sbz + kb, 128, L.sbo_z), bl = tc::desc(sbz + plz + kb, 128, L.sbo_z);
-            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (zb | s) ? 1u : 0u);
-            tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
-            tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
-          }
+        for (int s = 0; s < 4; ++s) {
+          const uint64_t bb = tc::desc(sbz + (uint32_t)(gi.zb * 4 + s) * 256, 128, L.sbo_z);
+          tc::mma_tf32_ts(d, a + 8 * s, bb, id64, (gi.zb | s) ? 1u : 0u);  // hi.[hi | lo]
+          tc::mma_tf32_ts(d, a + 32 + 8 * s, bb, id32, 1u);               // lo.hi
         }
         tc::commit(&az_empty[b]);
-        if (zb != L.nzb - 1) continue;
-        tc::commit(&d2_full[cb]);
-        // ---- stage Y for this chunk
-        tc::mbar_wait(&ay_full, chunk & 1);
+        if (gi.zb == L.nzb - 1) {
+          tc::commit(&d2_full[cb]);
+          ++chunk;
+        }
+        gi.next(L);
+      }
+    }
+  } else if (warp == kIssY) {
+    // ======================= stage Y issuer (A_Y in shared memory) =======================
+    if (lane == 0) {
+      const uint32_t id = tc::idesc_tf32(128, 32);
+      const uint32_t sby = tc::smem_u32(by), ply = 4 * L.sbo_y, say = tc::smem_u32(ay);
+      int slab_i = 0;
+      for (int c = 0; c < n_chunks; ++c) {
+        const int yc = c % L.nyc;
+        tc::mbar_wait(&ay_full, c & 1);
         if (yc == 0) tc::mbar_wait(&d3_empty, (slab_i & 1) ^ 1);
         tc::fence_after();
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t a = tmem + cAY + 32 * hh, d = tmem + cD3 + 32 * hh;
+          const uint32_t d = tmem + cD3 + 32 * hh;
+          const uint32_t a_hi = say + (2 * hh) * kAYPlane, a_lo = a_hi + kAYPlane;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             const uint32_t kb = (uint32_t)(yc * 2 + s) * 256;
             const uint64_t bh = tc::desc(sby + kb, 128, L.sbo_y), bl = tc::desc(sby + ply + kb, 128, L.sbo_y);
-            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (yc | s) ? 1u : 0u);
-            tc::mma_tf32_ts(d, a + 16 + 8 * s, bh, id, 1u);
-            tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+            const uint64_t ah = tc::desc(a_hi + s * 256, 128, 512), al = tc::desc(a_lo + s * 256, 128, 512);
+            tc::mma_tf32(d, ah, bh, id, (yc | s) ? 1u : 0u);
+            tc::mma_tf32(d, al, bh, id, 1u);
+            tc::mma_tf32(d, ah, bl, id, 1u);
           }
         }
         tc::commit(&ay_empty);
-        ++chunk;
         if (yc == L.nyc - 1) {
           tc::commit(&d3_full);
           ++slab_i;

@@ -174,13 +174,27 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
   return ok;
 }
 
-// Wait for the phase with the given parity to complete.  Watchdog: a wait
-// longer than ~2^35 cycles (tens of seconds) traps, turning a pipeline
-// deadlock into a launch error instead of a hung GPU.
+__device__ __forceinline__ uint32_t mbar_try_hint(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok;
+}
+
+// Wait for the phase with the given parity to complete.  try_wait suspends
+// the thread (up to a 1 ms hint) instead of spinning, so waiting warps do not
+// take issue slots from working warps.  Watchdog: a wait longer than ~2^35
+// cycles (tens of seconds) traps, turning a pipeline deadlock into a launch
+// error instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try(bar, parity)) return;
+  if (mbar_try_hint(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try(bar, parity)) {
+  while (!mbar_try_hint(bar, parity)) {
     if (clock64() - t0 > (1ll << 35)) __trap();
   }
 }
