@@ -35,6 +35,8 @@
 // Envelope: fp32, r_y, r_z, r_t <= 16, Nt % 4 == 0 (TMA stride rule), 16-byte
 // aligned inputs; the caller falls back to dft_yzt_tc.cu otherwise.
 #include <cuda.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -45,12 +47,12 @@ namespace {
 
 // warp roles
 constexpr int kConvW = 8;                 // converters: two sets of 4 (tile parity), one warp per TMEM quarter
-constexpr int kTepiW0 = 8;                // warps 8-11: D1 -> A_Z
-constexpr int kZepiW0 = 12;               // warps 12-15: D2 -> A_Y, D3 -> output
-constexpr int kTmaW = 16;                 // TMA producer
-constexpr int kIssT0 = 17, kIssT1 = 18;   // stage-T issuers (group parity when one t block per group)
-constexpr int kIssZ = 19, kIssY = 20;     // stage-Z / stage-Y issuers
-constexpr int kWarps = 21;
+constexpr int kTepiW0 = 8;                // warps 8-15: D1 -> A_Z, two sets of 4 (group parity)
+constexpr int kZepiW0 = 16;               // warps 16-19: D2 -> A_Y, D3 -> output
+constexpr int kTmaW = 20;                 // TMA producer
+constexpr int kIssT0 = 21, kIssT1 = 22;   // stage-T issuers (group parity when one t block per group)
+constexpr int kIssZ = 23, kIssY = 24;     // stage-Z / stage-Y issuers
+constexpr int kWarps = 25;
 constexpr int kThreads2 = kWarps * 32;
 constexpr int kTileBytes = 128 * 32 * 4;            // 128 rows x 32 t fp32
 constexpr int kScratchWarp = 2 * 2 * 16 * 17 * 4;   // [part][yy][kt][z (+1)]
@@ -85,7 +87,7 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.off_bt = o; o += 2 * 4 * L.sbo_t;   // hi, lo planes of 32 rows
   L.off_bz = o; o += 2 * 4 * L.sbo_z;
   L.off_by = o; o += 2 * 4 * L.sbo_y;
-  L.off_scr = o; o += 4 * kScratchWarp;
+  L.off_scr = o; o += 8 * kScratchWarp;
   L.off_stash = o; o += kStashBytes;
   o = (o + 1023) & ~1023;
   L.off_ay = o; o += kAYBytes;
@@ -141,8 +143,18 @@ struct GroupIdx {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
-                  const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap) {
+                  const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap,
+                  unsigned long long* __restrict__ prof, int exp) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
+  // optional wait profile (debug): per warp, cycles waiting in slots 0..3 and total
+  long long wt[4] = {0, 0, 0, 0};
+  const long long t_start = clock64();
+#define DFNO_W(slot, call)                        \
+  do {                                            \
+    const long long t0_ = clock64();              \
+    call;                                         \
+    if (prof) wt[slot] += clock64() - t0_;         \
+  } while (0)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[4], empty[4], at_full[2], at_empty[2], d1_full[2], d1_empty[2];
@@ -198,7 +210,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::mbar_init(&at_full[b], 128);
       tc::mbar_init(&at_empty[b], 1);
       tc::mbar_init(&d1_full[b], 1);
-      tc::mbar_init(&d1_empty[b], 128);
+      tc::mbar_init(&d1_empty[b], 128);  // T-epilogue set b
       tc::mbar_init(&az_full[b], 128);
       tc::mbar_init(&az_empty[b], 1);
       tc::mbar_init(&d2_full[b], 1);
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int sw = r & 7;
     for (int i = set; i < n_tiles; i += 2) {
       const int s = i % S, n = i / S;
-      tc::mbar_wait(&full[s], n & 1);
+      DFNO_W(0, tc::mbar_wait_lazy(&full[s], n & 1, 32));
       const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
       const int b = i & 1;
 #pragma unroll
@@ -249,7 +261,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           tc::split_hl(conv<MODE, ACT>(q.z, p.z), h[4 * c4 + 2], l[4 * c4 + 2]);
           tc::split_hl(conv<MODE, ACT>(q.w, p.w), h[4 * c4 + 3], l[4 * c4 + 3]);
         }
-        if (half == 0) tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
+        if (half == 0) DFNO_W(1, tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1));
         tc::tmem_st16(tmem + cAT + 64 * b + 16 * half + quarter_off, h);
         tc::tmem_st16(tmem + cAT + 64 * b + 32 + 16 * half + quarter_off, l);
       }
@@ -260,12 +272,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
   } else if (warp < kZepiW0) {
     // ======================= T epilogue: D1 -> A_Z =======================
-    const int q = warp - kTepiW0;
-    float* scr = reinterpret_cast<float*>(smem + L.off_scr + q * kScratchWarp);  // [part][yy][kt][17]
+    const int set = (warp - kTepiW0) >> 2;
+    float* scr = reinterpret_cast<float*>(smem + L.off_scr + (warp - kTepiW0) * kScratchWarp);  // [part][yy][kt][17]
     const int yy = lane >> 4, lo16 = lane & 15;
-    for (int G = 0; G < n_groups; ++G) {
+    for (int G = set; G < n_groups; G += 2) {
       const int b = G & 1;
-      tc::mbar_wait(&d1_full[b], (G >> 1) & 1);
+      DFNO_W(0, tc::mbar_wait(&d1_full[b], (G >> 1) & 1));
       tc::fence_after();
       uint32_t u[32];
       tc::tmem_ld32_nowait(tmem + cD1 + 32 * b + quarter_off, u);
@@ -278,17 +290,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
         scr[((1 * 2 + yy) * 16 + kt) * 17 + lo16] = __uint_as_float(u[16 + kt]);
       }
       __syncwarp();
-      float h[32], l[32];
+      DFNO_W(1, tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1));
+      tc::fence_after();
 #pragma unroll
-      for (int z = 0; z < 16; ++z) {
-        tc::split_hl(scr[((0 * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
-        tc::split_hl(scr[((1 * 2 + yy) * 16 + lo16) * 17 + z], h[16 + z], l[16 + z]);
+      for (int part = 0; part < 2; ++part) {  // A_Z cols: hi re | hi im | lo re | lo im
+        float h[16], l[16];
+#pragma unroll
+        for (int z = 0; z < 16; ++z) tc::split_hl(scr[((part * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
+        tc::tmem_st16(tmem + cAZ + 64 * b + 16 * part + quarter_off, h);
+        tc::tmem_st16(tmem + cAZ + 64 * b + 32 + 16 * part + quarter_off, l);
       }
       __syncwarp();
-      tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1);
-      tc::fence_after();
-      tc::tmem_st32(tmem + cAZ + 64 * b + quarter_off, h);
-      tc::tmem_st32(tmem + cAZ + 64 * b + 32 + quarter_off, l);
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&az_full[b]);
@@ -302,7 +314,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     int slab_i = 0;
     for (int c = 0; c < n_chunks; ++c) {
       const int yc = c % L.nyc, cb = c & 1;
-      tc::mbar_wait(&d2_full[cb], (c >> 1) & 1);
+      DFNO_W(0, tc::mbar_wait_lazy(&d2_full[cb], (c >> 1) & 1));
       tc::fence_after();
       uint32_t u0[32];
       {
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
       }
       tc::named_sync(1, 128);
-      tc::mbar_wait(&ay_empty, (c & 1) ^ 1);
+      DFNO_W(1, tc::mbar_wait_lazy(&ay_empty, (c & 1) ^ 1));
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         // A_Y tile hh row (kz_l, kt), K = (re y0..7, im y0..7), hi / lo planes,
@@ -351,7 +363,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       // ---- slab end: D3 -> XK exchange layout
       const int slab = (int)blockIdx.x + slab_i * (int)gridDim.x;
       const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
-      tc::mbar_wait(&d3_full, slab_i & 1);
+      DFNO_W(2, tc::mbar_wait_lazy(&d3_full, slab_i & 1));
       tc::fence_after();
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
@@ -380,7 +392,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       for (int i = 0; i < n_tiles; ++i) {
         const int s = i % S, n = i / S;
         const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
-        tc::mbar_wait(&empty[s], (n & 1) ^ 1);
+        DFNO_W(0, tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64));
         tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
         unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
         tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
@@ -399,10 +411,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const uint32_t sbt = tc::smem_u32(bt), plt = 4 * L.sbo_t;
       for (int G = two_t ? k : 0; G < n_groups; G += two_t ? 2 : 1) {
         const int b = G & 1;
-        tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1);
+        DFNO_W(0, tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1));
         for (int tb = 0; tb < L.ntb; ++tb) {
           const int i = G * L.ntb + tb, ab = i & 1;
-          tc::mbar_wait(&at_full[ab], (i >> 1) & 1);
+          DFNO_W(1, tc::mbar_wait(&at_full[ab], (i >> 1) & 1));
           tc::fence_after();
           const uint32_t a = tmem + cAT + 64 * ab, d = tmem + cD1 + 32 * b;
 #pragma unroll
@@ -427,8 +439,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
       int chunk = 0;
       for (int G = 0; G < n_groups; ++G) {
         const int b = G & 1, cb = chunk & 1;
-        tc::mbar_wait(&az_full[b], (G >> 1) & 1);
-        if (gi.zb == 0) tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1);
+        DFNO_W(0, tc::mbar_wait(&az_full[b], (G >> 1) & 1));
+        if (gi.zb == 0) DFNO_W(1, tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1));
         tc::fence_after();
         const uint32_t a = tmem + cAZ + 64 * b, d = tmem + cD2 + 64 * cb;
 #pragma unroll
@@ -453,8 +465,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
       int slab_i = 0;
       for (int c = 0; c < n_chunks; ++c) {
         const int yc = c % L.nyc;
-        tc::mbar_wait(&ay_full, c & 1);
-        if (yc == 0) tc::mbar_wait(&d3_empty, (slab_i & 1) ^ 1);
+        DFNO_W(0, tc::mbar_wait_lazy(&ay_full, c & 1, 64));
+        if (yc == 0) DFNO_W(1, tc::mbar_wait_lazy(&d3_empty, (slab_i & 1) ^ 1, 64));
         tc::fence_after();
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -478,6 +490,15 @@ __global__ void __launch_bounds__(kThreads2, 1)
       }
     }
   }
+  if (prof && lane == 0) {
+    const long long tot = clock64() - t_start;
+    atomicAdd(prof + warp * 5 + 0, (unsigned long long)wt[0]);
+    atomicAdd(prof + warp * 5 + 1, (unsigned long long)wt[1]);
+    atomicAdd(prof + warp * 5 + 2, (unsigned long long)wt[2]);
+    atomicAdd(prof + warp * 5 + 3, (unsigned long long)wt[3]);
+    atomicAdd(prof + warp * 5 + 4, (unsigned long long)tot);
+  }
+#undef DFNO_W
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -540,8 +561,22 @@ int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, 
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int grid = sm_count2() < slabs ? sm_count2() : slabs;
-  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap);
+  static unsigned long long* prof = nullptr;
+  static const bool want_prof = getenv("DFNO_WAIT_PROFILE") && getenv("DFNO_WAIT_PROFILE")[0] == '1';
+  if (want_prof && !prof) cudaMalloc(&prof, kWarps * 5 * sizeof(unsigned long long));
+  if (prof) cudaMemsetAsync(prof, 0, kWarps * 5 * sizeof(unsigned long long), st);
+  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap, prof);
   DFNO_CUDA_CHECK_LAUNCH();
+  if (prof) {  // debug: per-warp wait cycles summed over CTAs
+    unsigned long long h[kWarps * 5];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "yzt_fwd_tc2 mode %d: per-CTA avg cycles  [w0 w1 w2 w3 | total]\n", MODE);
+    for (int w = 0; w < kWarps; ++w)
+      fprintf(stderr, "  warp %2d: %9.0f %9.0f %9.0f %9.0f | %9.0f\n", w, h[w * 5] / (double)grid,
+              h[w * 5 + 1] / (double)grid, h[w * 5 + 2] / (double)grid, h[w * 5 + 3] / (double)grid,
+              h[w * 5 + 4] / (double)grid);
+  }
   return DFNO_OK;
 }
 

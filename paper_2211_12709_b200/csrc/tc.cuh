@@ -187,15 +187,24 @@ __device__ __forceinline__ uint32_t mbar_try_hint(uint64_t* bar, uint32_t parity
 }
 
 // Wait for the phase with the given parity to complete.  try_wait suspends
-// the thread (up to a 1 ms hint) instead of spinning, so waiting warps do not
-// take issue slots from working warps.  Watchdog: a wait longer than ~2^35
-// cycles (tens of seconds) traps, turning a pipeline deadlock into a launch
-// error instead of a hung GPU.
+// the thread for a hardware-bounded time instead of spinning.  Watchdog: ~2^28
+// failed polls (seconds) trap, turning a pipeline deadlock into a launch error
+// instead of a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_hint(bar, parity)) return;
-  const long long t0 = clock64();
+  uint32_t n = 0;
   while (!mbar_try_hint(bar, parity)) {
-    if (clock64() - t0 > (1ll << 35)) __trap();
+    if (++n > (1u << 28)) __trap();
+  }
+}
+
+// Same, for roles off the critical path (long waits): back off with
+// nanosleep between polls so the waiting warp leaves its issue slots to the
+// warps doing work.
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, uint32_t ns = 128) {
+  uint32_t n = 0;
+  while (!mbar_try_hint(bar, parity)) {
+    __nanosleep(ns);
+    if (++n > (1u << 26)) __trap();
   }
 }
 

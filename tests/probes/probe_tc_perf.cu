@@ -326,3 +326,83 @@ extern "C" int probe_lean_run(int which, int R, long long* cyc) {
     default: return -1;
   }
 }
+
+// Contention probe: warp 0 issues R x 8 TS MMAs (N = 32) while warps 1..W-1
+// run a background load (bg: 0 none, 1 FFMA chains, 2 tcgen05.ld of their
+// quarter, 3 tcgen05.st to their quarter) until the MMAs complete.
+__global__ void probe_contention(int R, int bg, long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ volatile int done;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  for (int e = tid; e < 16 * 1024 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(smem)[e] = 0x3f800000u;
+  if (warp == 0) tc::tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+    done = 0;
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
+  constexpr uint32_t idesc = tc::idesc_tf32(128, 32);
+  const uint64_t db = tc::desc(tc::smem_u32(smem), 128, 256);
+  if (warp == 0) {
+    const long long t0 = clock64();
+    if (lane == 0) {
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tm + 32 * (j & 3)),
+              "r"(tm + 256 + 8 * (j & 1)), "l"(db + (uint64_t)((j & 1) * 16)), "n"(idesc), "r"(1));
+      }
+      tc::commit(&bar);
+    }
+    __syncwarp();
+    tc::mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (lane == 0) {
+      cyc[0] = t1 - t0;
+      done = 1;
+    }
+  } else {
+    float x = (float)tid, y = 1.0001f;
+    uint32_t acc = 0;
+    while (!done) {
+      if (bg == 1) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) x = fmaf(x, y, 0.5f);
+      } else if (bg == 2) {
+        uint32_t r[32];
+        tc::tmem_ld32_nowait(tm + 384 + lane_off, r);
+        tc::tmem_ld_wait();
+        acc += r[lane];
+      } else if (bg == 3) {
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = x + k;
+        tc::tmem_st32(tm + 448 + lane_off, v);
+        tc::tmem_st_wait();
+      } else {
+        __nanosleep(100);
+      }
+    }
+    if (x == 0.f && acc == 7) cyc[1] = 1;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tm);
+}
+
+extern "C" int probe_contention_run(int R, int bg, int warps, long long* cyc) {
+  cudaFuncSetAttribute(probe_contention, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 1024);
+  probe_contention<<<1, 32 * warps, 16 * 1024>>>(R, bg, cyc);
+  return (int)cudaDeviceSynchronize();
+}

@@ -160,3 +160,17 @@ def test_tcgen05_lean_issue_report(perf):
     for i, n in enumerate(names):
         assert perf.probe_lean_run(i, 64, ctypes.c_void_p(cyc.data_ptr())) == 0
         print(f"lean tf32 M=128 {n}: {int(cyc[0]) / (8 * 64):6.1f} cyc/MMA")
+
+
+def test_tcgen05_issue_under_contention_report(perf):
+    a = torch.randn(4096, 4096, device="cuda")
+    for _ in range(50):
+        a = a @ a
+        a /= a.norm()
+    torch.cuda.synchronize()
+    cyc = torch.zeros(2, dtype=torch.int64, device="cuda")
+    R = 64
+    for bg, name in ((0, "idle"), (1, "FFMA"), (2, "tcgen05.ld"), (3, "tcgen05.st")):
+        for warps in (2, 8, 24):
+            assert perf.probe_contention_run(R, bg, warps, ctypes.c_void_p(cyc.data_ptr())) == 0
+            print(f"TS N=32 MMA issue, {warps - 1:2d} background warps ({name:10s}): {int(cyc[0]) / (8 * R):6.1f} cyc/MMA")
