@@ -144,7 +144,7 @@ template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
                   const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap,
-                  unsigned long long* __restrict__ prof, int exp) {
+                  unsigned long long* __restrict__ prof) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
   // optional wait profile (debug): per warp, cycles waiting in slots 0..3 and total
   long long wt[4] = {0, 0, 0, 0};
