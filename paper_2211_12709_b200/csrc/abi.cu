@@ -19,6 +19,7 @@ int yzt_fwd_tc(const dfno_geom&, const void*, const void*, int, double, void*, c
 int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
 // TMEM-operand tcgen05 path (dft_fwd_tc.cu)
 int yzt_fwd_tc2(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
+int yzt_inv_tc2(const dfno_geom&, const void*, double, void*, cudaStream_t);
 }  // namespace dfno
 
 using namespace dfno;
@@ -143,6 +144,11 @@ extern "C" int dfno_dft_yzt_inv(const dfno_geom* g, const void* xk_in, double sc
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) {
     if (tc_enabled()) {
+      static const bool v1 = env_flag("DFNO_YZT_V1");
+      if (!v1) {
+        rc = yzt_inv_tc2(*g, xk_in, scale, out, st);
+        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+      }
       rc = yzt_inv_tc(*g, xk_in, scale, out, st);
       if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     }
