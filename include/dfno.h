@@ -172,6 +172,21 @@ int dfno_xspec_fwd(const dfno_geom* g, const void* kx_in, const void* w,
 int dfno_xspec_bwd(const dfno_geom* g, const void* kx_in, const void* spec,
                    const void* w, void* gw, void* kx_out, void* stream);
 
+/*
+ * Workspace variants of the x-spectral stage: the DFT along x, the per-mode
+ * channel contraction and the inverse DFT run as three bandwidth-shaped
+ * kernels with the truncated spectra staged in `work` (caller-owned device
+ * memory of dfno_xspec_workspace() bytes).  Same results and reference lines
+ * as dfno_xspec_fwd / dfno_xspec_bwd; fp32 with batch <= 4 (other cases fall
+ * back to the fused kernel, `work` unused).
+ */
+int dfno_xspec_workspace(const dfno_geom* g, int64_t* bytes);
+int dfno_xspec_fwd_ws(const dfno_geom* g, const void* kx_in, const void* w,
+                      void* spec, void* kx_out, void* work, void* stream);
+int dfno_xspec_bwd_ws(const dfno_geom* g, const void* kx_in, const void* spec,
+                      const void* w, void* gw, void* kx_out, void* work,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ EXPORTS = (
     "dfno_abi_version", "dfno_status_string", "dfno_build_info", "dfno_geom_validate", "dfno_sizes",
     "dfno_mix_fwd", "dfno_mix_bwd_partials", "dfno_mix_bwd", "dfno_reduce_partials",
     "dfno_dft_yzt_fwd", "dfno_dft_yzt_inv", "dfno_xspec_fwd", "dfno_xspec_bwd",
+    "dfno_xspec_workspace", "dfno_xspec_fwd_ws", "dfno_xspec_bwd_ws",
 )
 
 
@@ -88,6 +89,9 @@ def load(path: Path = LIB_PATH) -> ctypes.CDLL:
         "dfno_dft_yzt_inv": ([gp, vp, dbl, vp, vp], i32),
         "dfno_xspec_fwd": ([gp, vp, vp, vp, vp, vp], i32),
         "dfno_xspec_bwd": ([gp, vp, vp, vp, vp, vp, vp], i32),
+        "dfno_xspec_workspace": ([gp, ctypes.POINTER(i64)], i32),
+        "dfno_xspec_fwd_ws": ([gp, vp, vp, vp, vp, vp, vp], i32),
+        "dfno_xspec_bwd_ws": ([gp, vp, vp, vp, vp, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -20,6 +20,10 @@ int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
 // TMEM-operand tcgen05 path (dft_fwd_tc.cu)
 int yzt_fwd_tc2(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
 int yzt_inv_tc2(const dfno_geom&, const void*, double, void*, cudaStream_t);
+// streamed x-spectral stage (xspec_stream.cu)
+size_t xspec_stream_workspace(const dfno_geom&);
+int xspec_fwd_stream(const dfno_geom&, const void*, const void*, void*, void*, void*, cudaStream_t);
+int xspec_bwd_stream(const dfno_geom&, const void*, const void*, const void*, void*, void*, void*, cudaStream_t);
 }  // namespace dfno
 
 using namespace dfno;
@@ -177,4 +181,34 @@ extern "C" int dfno_xspec_bwd(const dfno_geom* g, const void* kx_in, const void*
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) return xspec_bwd_simt<float>(*g, kx_in, spec, w, gw, kx_out, st);
   return xspec_bwd_simt<double>(*g, kx_in, spec, w, gw, kx_out, st);
+}
+
+extern "C" int dfno_xspec_workspace(const dfno_geom* g, int64_t* bytes) {
+  if (!g || !bytes) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  *bytes = (int64_t)xspec_stream_workspace(*g);
+  return DFNO_OK;
+}
+
+extern "C" int dfno_xspec_fwd_ws(const dfno_geom* g, const void* kx_in, const void* w, void* spec, void* kx_out,
+                                 void* work, void* stream) {
+  if (!g || !kx_in || !w || !kx_out || !work) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  const int r2 = xspec_fwd_stream(*g, kx_in, w, spec, kx_out, work, (cudaStream_t)stream);
+  if (r2 != DFNO_ERR_UNSUPPORTED) return r2;
+  return dfno_xspec_fwd(g, kx_in, w, spec, kx_out, stream);
+}
+
+extern "C" int dfno_xspec_bwd_ws(const dfno_geom* g, const void* kx_in, const void* spec, const void* w, void* gw,
+                                 void* kx_out, void* work, void* stream) {
+  if (!g || !kx_in || !spec || !w || !gw || !kx_out || !work) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  const int r2 = xspec_bwd_stream(*g, kx_in, spec, w, gw, kx_out, work, (cudaStream_t)stream);
+  if (r2 != DFNO_ERR_UNSUPPORTED) return r2;
+  return dfno_xspec_bwd(g, kx_in, spec, w, gw, kx_out, stream);
 }

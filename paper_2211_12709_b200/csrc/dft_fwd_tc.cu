@@ -40,6 +40,7 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "tmap.cuh"
 
 namespace dfno {
 
@@ -532,18 +533,6 @@ int smem_optin() {
   return n;
 }
 
-// 4-D map over (t, z, y, slab) of a (slabs, Ny, Nz, Nt) fp32 tensor, box
-// (32, 16, 8, 1), 128-byte swizzle, out-of-bounds zero fill.
-bool make_map(CUtensorMap* m, const void* base, int ny, int nz, int nt, int slabs) {
-  cuuint64_t dims[4] = {(cuuint64_t)nt, (cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)slabs};
-  cuuint64_t strides[3] = {(cuuint64_t)nt * 4, (cuuint64_t)nz * nt * 4, (cuuint64_t)ny * nz * nt * 4};
-  cuuint32_t box[4] = {32, 16, 8, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box,
-                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int MODE, int ACT>
 int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, void* out, cudaStream_t st) {
   const int cap = smem_optin();
@@ -551,9 +540,9 @@ int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, 
   if (L.stages < 2) return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   CUtensorMap ms, mp;
-  if (!make_map(&ms, src, g.ny, g.nz, g.nt, slabs)) return DFNO_ERR_UNSUPPORTED;
+  if (!make_slab_map(&ms, src, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) return DFNO_ERR_UNSUPPORTED;
   if (MODE == DFNO_SRC_GRAD) {
-    if (!make_map(&mp, pre, g.ny, g.nz, g.nt, slabs)) return DFNO_ERR_UNSUPPORTED;
+    if (!make_slab_map(&mp, pre, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) return DFNO_ERR_UNSUPPORTED;
   } else {
     mp = ms;
   }

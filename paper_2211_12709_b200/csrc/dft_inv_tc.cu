@@ -32,6 +32,7 @@
 
 #include "common.cuh"
 #include "tc.cuh"
+#include "tmap.cuh"
 
 namespace dfno {
 
@@ -476,16 +477,6 @@ int smem_cap_i() {
   return n;
 }
 
-bool make_out_map(CUtensorMap* m, void* base, int ny, int nz, int nt, int slabs) {
-  cuuint64_t dims[4] = {(cuuint64_t)nt, (cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)slabs};
-  cuuint64_t strides[3] = {(cuuint64_t)nt * 4, (cuuint64_t)nz * nt * 4, (cuuint64_t)ny * nz * nt * 4};
-  cuuint32_t box[4] = {32, 16, 8, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 }  // namespace
 
 int yzt_inv_tc2(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
@@ -495,7 +486,7 @@ int yzt_inv_tc2(const dfno_geom& g, const void* in, double scale, void* out, cud
   if (L.total > smem_cap_i()) return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   CUtensorMap mo;
-  if (!make_out_map(&mo, out, g.ny, g.nz, g.nt, slabs)) return DFNO_ERR_UNSUPPORTED;
+  if (!make_slab_map(&mo, out, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_NONE)) return DFNO_ERR_UNSUPPORTED;
   if (cudaFuncSetAttribute(k_yzt_inv_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) !=
       cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;

@@ -1,0 +1,41 @@
+// Tensor-map (TMA descriptor) encoding without a link-time dependency on
+// libcuda: cuTensorMapEncodeTiled is resolved through the runtime's driver
+// entry-point query, so libdfno.so still loads (and its host-only entry
+// points work) on machines without a GPU driver.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+namespace dfno {
+
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 4-D fp32 map over (t, z, y, slab) of a (slabs, Ny, Nz, Nt) tensor, box
+// (32, 16, 8, 1), 128-byte swizzle, out-of-bounds elements zero-filled on
+// load and dropped on store.
+inline bool make_slab_map(CUtensorMap* m, const void* base, int ny, int nz, int nt, int slabs,
+                          CUtensorMapL2promotion l2) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)nt, (cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)slabs};
+  cuuint64_t strides[3] = {(cuuint64_t)nt * 4, (cuuint64_t)nz * nt * 4, (cuuint64_t)ny * nz * nt * 4};
+  cuuint32_t box[4] = {32, 16, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+}  // namespace dfno

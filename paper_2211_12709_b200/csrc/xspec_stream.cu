@@ -1,0 +1,275 @@
+// x-spectral stage as three bandwidth-shaped kernels (fp32), the path used
+// when the caller supplies a workspace (dfno_xspec_fwd_ws / _bwd_ws):
+//
+//   k_xdft    X[b][c][kx][m] = s1 * sum_x Z[b][c][x][m] e^{-2 pi i kx x/Nx}
+//             (Z gathered straight from the peer-major KX exchange buffer:
+//             unpack fused; truncation implicit -- only retained kx rows of
+//             the twiddle table exist)                     d/fno.py:331-332
+//   k_xmix    forward  Y[b][o][kx][m] = sum_i X[b][i][kx][m] W[i][o][kx][m]
+//             (d/tensor.py:231-255): a batched small GEMM per (kx, m), bound
+//             by the weight stream (8 flop per 8 B at b = 1), so each thread
+//             owns one (o group, kx, m) column: every W load is a coalesced
+//             256-byte warp transaction and every W byte is read once.
+//   k_xmix_bwd gW[i][o][kx][m] = sum_b conj(S[b][i]) D[b][o]
+//             dX[b][i][kx][m]  = sum_o D[b][o] conj(W[i][o])  (d/fno.py:415-423)
+//   k_xidft   U[b][c][x][m] = s2 * sum_kx Y[b][c][kx][m] e^{+2 pi i kx x/Nx}
+//             written straight into the KX layout (pack fused; zero padding
+//             of the missing kx implicit)                  d/fno.py:335-336
+//
+// Compared with the fused one-CTA-per-mode-block kernel (xspec.cu) this
+// streams the weights with full occupancy and no block-wide phases; the
+// extra traffic is the 2 x b c r_x (ky) r_z r_t spectrum round trip
+// (21 MB at C2 against 210 MB of weights).
+#include "common.cuh"
+
+namespace dfno {
+
+namespace {
+constexpr int kXT = 256;  // threads per block
+constexpr int kOG = 4;    // output channels per thread in k_xmix / input channels in k_xmix_bwd
+constexpr int kBMax = 4;  // batch entries held in registers by k_xmix_bwd
+
+__device__ __forceinline__ long long mloc_of(const dfno_geom& g) { return (long long)ky_local(g) * g.rz * g.rt; }
+
+// twiddle table tw[x][kx] = e^{-2 pi i f(kx) x / Nx} in shared memory
+__device__ void fill_tw(float2* tw, const dfno_geom& g) {
+  for (int e = threadIdx.x; e < g.nx * g.rx; e += blockDim.x) {
+    const int x = e / g.rx, k = e % g.rx;
+    tw[e] = twiddle<float>(mode_freq(k, g.nx, g.mx), x, g.nx, -1);
+  }
+  __syncthreads();
+}
+}  // namespace
+
+// one thread per (b, c, m) column; RXM >= rx register accumulators
+template <int RXM>
+__global__ void __launch_bounds__(kXT) k_xdft(const dfno_geom g, const float2* __restrict__ kx_in, float s1,
+                                              float2* __restrict__ X) {
+  extern __shared__ float2 tw[];
+  fill_tw(tw, g);
+  const long long mloc = mloc_of(g);
+  const long long n = (long long)g.batch * g.c * mloc;
+  const int rx = g.rx;
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long m = e % mloc, bc = e / mloc;
+    const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
+    float2 acc[RXM];
+#pragma unroll
+    for (int k = 0; k < RXM; ++k) acc[k] = make_float2(0.f, 0.f);
+    for (int p = 0; p < g.nranks; ++p) {  // peer chunks of the KX layout (d/partition.py:135-188)
+      const int x0 = g.x_starts[p], x1 = g.x_starts[p + 1];
+      const float2* src = kx_in + kx_row(g, bb, c, x0) + m;
+#pragma unroll 4
+      for (int x = x0; x < x1; ++x) {
+        const float2 z = __ldcs(src);
+        src += mloc;
+        const float2* t = tw + x * rx;
+#pragma unroll
+        for (int k = 0; k < RXM; ++k)
+          if (k < rx) cmac<float>(acc[k], z, t[k]);
+      }
+    }
+    float2* dst = X + (bc * rx) * mloc + m;
+#pragma unroll
+    for (int k = 0; k < RXM; ++k)
+      if (k < rx) dst[(long long)k * mloc] = make_float2(s1 * acc[k].x, s1 * acc[k].y);
+  }
+}
+
+// one thread per (b, c, m) column: all Nx outputs
+template <int RXM>
+__global__ void __launch_bounds__(kXT) k_xidft(const dfno_geom g, const float2* __restrict__ Y, float s2,
+                                               float2* __restrict__ kx_out) {
+  extern __shared__ float2 tw[];
+  fill_tw(tw, g);
+  const long long mloc = mloc_of(g);
+  const long long n = (long long)g.batch * g.c * mloc;
+  const int rx = g.rx;
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long m = e % mloc, bc = e / mloc;
+    const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
+    float2 yv[RXM];
+    const float2* src = Y + (bc * rx) * mloc + m;
+#pragma unroll
+    for (int k = 0; k < RXM; ++k) yv[k] = (k < rx) ? src[(long long)k * mloc] : make_float2(0.f, 0.f);
+    for (int p = 0; p < g.nranks; ++p) {
+      const int x0 = g.x_starts[p], x1 = g.x_starts[p + 1];
+      float2* dst = kx_out + kx_row(g, bb, c, x0) + m;
+#pragma unroll 2
+      for (int x = x0; x < x1; ++x) {
+        const float2* t = tw + x * rx;
+        float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < RXM; ++k)
+          if (k < rx) cmac_conj_b<float>(a, yv[k], t[k]);  // e^{+i} = conj(e^{-i})
+        __stcs(dst, make_float2(s2 * a.x, s2 * a.y));
+        dst += mloc;
+      }
+    }
+  }
+}
+
+// forward contraction: one thread per (o group, kx, m), all batch entries
+__global__ void __launch_bounds__(kXT) k_xmix(const dfno_geom g, const float2* __restrict__ X,
+                                              const float2* __restrict__ W, float2* __restrict__ Y) {
+  const long long mloc = mloc_of(g);
+  const int rx = g.rx, C = g.c, nog = (C + kOG - 1) / kOG;
+  const long long cols = (long long)rx * mloc;  // (kx, m)
+  const long long n = (long long)nog * cols;
+  const long long wo = cols;                    // W stride between consecutive o
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long col = e % cols;
+    const int o0 = (int)(e / cols) * kOG;
+    for (int bb = 0; bb < g.batch; ++bb) {
+      float2 acc[kOG];
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) acc[j] = make_float2(0.f, 0.f);
+      const float2* xp = X + ((long long)bb * C) * cols + col;
+      const float2* wp = W + ((long long)o0) * wo + col;
+#pragma unroll 2
+      for (int i = 0; i < C; ++i) {
+        const float2 xv = xp[(long long)i * cols];
+        const float2* wr = wp + (long long)i * C * wo;
+        float2 wv[kOG];
+#pragma unroll
+        for (int j = 0; j < kOG; ++j) wv[j] = (o0 + j < C) ? __ldcs(wr + j * wo) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < kOG; ++j) cmac<float>(acc[j], xv, wv[j]);
+      }
+      float2* yp = Y + ((long long)bb * C + o0) * cols + col;
+#pragma unroll
+      for (int j = 0; j < kOG; ++j)
+        if (o0 + j < C) yp[j * cols] = acc[j];
+    }
+  }
+}
+
+// backward contraction: one thread per (i group, kx, m); batch <= BM <= kBMax
+template <int BM>
+__global__ void __launch_bounds__(kXT) k_xmix_bwd(const dfno_geom g, const float2* __restrict__ S,
+                                                  const float2* __restrict__ D, const float2* __restrict__ W,
+                                                  float2* __restrict__ gW, float2* __restrict__ dX) {
+  const long long mloc = mloc_of(g);
+  const int rx = g.rx, C = g.c, nig = (C + kOG - 1) / kOG, B = g.batch;
+  const long long cols = (long long)rx * mloc;
+  const long long n = (long long)nig * cols;
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long col = e % cols;
+    const int i0 = (int)(e / cols) * kOG;
+    float2 sv[BM][kOG], dx[BM][kOG];
+#pragma unroll
+    for (int bb = 0; bb < BM; ++bb)
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) {
+        sv[bb][j] = (bb < B && i0 + j < C) ? S[((long long)bb * C + i0 + j) * cols + col] : make_float2(0.f, 0.f);
+        dx[bb][j] = make_float2(0.f, 0.f);
+      }
+#pragma unroll 2
+    for (int o = 0; o < C; ++o) {
+      float2 dv[BM];
+#pragma unroll
+      for (int bb = 0; bb < BM; ++bb) dv[bb] = (bb < B) ? D[((long long)bb * C + o) * cols + col] : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) {
+        if (i0 + j >= C) continue;
+        const long long wi = ((long long)(i0 + j) * C + o) * cols + col;
+        const float2 wv = __ldcs(W + wi);
+        float2 gacc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int bb = 0; bb < BM; ++bb) {
+          cmac_conj_a<float>(gacc, sv[bb][j], dv[bb]);   // conj(S) D
+          cmac_conj_b<float>(dx[bb][j], dv[bb], wv);     // D conj(W)
+        }
+        __stcs(gW + wi, gacc);
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < BM; ++bb)
+#pragma unroll
+      for (int j = 0; j < kOG; ++j)
+        if (bb < B && i0 + j < C) dX[((long long)bb * C + i0 + j) * cols + col] = dx[bb][j];
+  }
+}
+
+namespace {
+int sms_x() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+unsigned grid_for(long long n) {
+  long long b = (n + kXT - 1) / kXT;
+  const long long cap = (long long)sms_x() * 8;
+  return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
+  const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
+  const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
+  auto k = g.rx <= 16 ? k_xdft<16> : k_xdft<32>;
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
+  const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
+  const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
+  auto k = g.rx <= 16 ? k_xidft<16> : k_xidft<32>;
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+bool stream_ok(const dfno_geom& g) {
+  return g.dtype == DFNO_F32 && g.rx <= 32 && (size_t)g.nx * g.rx * sizeof(float2) <= 200 * 1024 &&
+         g.batch <= kBMax;
+}
+}  // namespace
+
+size_t xspec_stream_workspace(const dfno_geom& g) {
+  return 2 * (size_t)g.batch * g.c * g.rx * ky_local(g) * g.rz * g.rt * sizeof(float2);
+}
+
+int xspec_fwd_stream(const dfno_geom& g, const void* kx_in, const void* w, void* spec, void* kx_out, void* work,
+                     cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
+  const size_t half = xspec_stream_workspace(g) / 2;
+  void* X = spec ? spec : work;
+  void* Y = static_cast<char*>(work) + half;
+  int rc = launch_dft(g, kx_in, 1.f, X, st);  // fft_x unnormalised (d/spectral.py:36)
+  if (rc) return rc;
+  const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
+  k_xmix<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(g, (const float2*)X,
+                                                                              (const float2*)w, (float2*)Y);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return launch_idft(g, Y, (float)(1.0 / g.nx), kx_out, st);  // ifft_x carries 1/Nx (d/spectral.py:49)
+}
+
+int xspec_bwd_stream(const dfno_geom& g, const void* kx_in, const void* spec, const void* w, void* gw, void* kx_out,
+                     void* work, cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
+  const size_t half = xspec_stream_workspace(g) / 2;
+  void* D = work;
+  void* dX = static_cast<char*>(work) + half;
+  int rc = launch_dft(g, kx_in, (float)(1.0 / g.nx), D, st);  // fft_x / Nx (d/fno.py:450-452)
+  if (rc) return rc;
+  const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
+  auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
+  kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(
+      g, (const float2*)spec, (const float2*)D, (const float2*)w, (float2*)gw, (float2*)dX);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return launch_idft(g, dX, 1.f, kx_out, st);  // ifft_x * Nx = unnormalised inverse (d/fno.py:455-457)
+}
+
+}  // namespace dfno

@@ -371,6 +371,9 @@ class _Plan:
         self.buf_b = torch.empty(self.kx_elems, dtype=self.cplx, device=device)   # KX recv
         self.buf_c = torch.empty(self.kx_elems, dtype=self.cplx, device=device)   # KX send
         del n
+        ws = ctypes.c_int64()
+        _lib.check(self.lib.dfno_xspec_workspace(self.gp, ctypes.byref(ws)), "xspec workspace")
+        self.xspec_work = torch.empty(max(1, ws.value), dtype=torch.uint8, device=device)
         self.partials = {}
 
     # -- shapes ----------------------------------------------------------
@@ -417,14 +420,14 @@ class _Plan:
             self.gp, _lib.ptr(xk_in), float(scale), _lib.ptr(out), _lib.stream_handle()), "dfno_dft_yzt_inv"))
 
     def xspec_fwd(self, kx_in, w, spec, kx_out):
-        _launch("xspec_fwd", lambda: _lib.check(self.lib.dfno_xspec_fwd(
-            self.gp, _lib.ptr(kx_in), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(kx_out), _lib.stream_handle()),
-            "dfno_xspec_fwd"))
+        _launch("xspec_fwd", lambda: _lib.check(self.lib.dfno_xspec_fwd_ws(
+            self.gp, _lib.ptr(kx_in), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(kx_out), _lib.ptr(self.xspec_work),
+            _lib.stream_handle()), "dfno_xspec_fwd_ws"))
 
     def xspec_bwd(self, kx_in, spec, w, gw, kx_out):
-        _launch("xspec_bwd", lambda: _lib.check(self.lib.dfno_xspec_bwd(
+        _launch("xspec_bwd", lambda: _lib.check(self.lib.dfno_xspec_bwd_ws(
             self.gp, _lib.ptr(kx_in), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw), _lib.ptr(kx_out),
-            _lib.stream_handle()), "dfno_xspec_bwd"))
+            _lib.ptr(self.xspec_work), _lib.stream_handle()), "dfno_xspec_bwd_ws"))
 
     # -- exchanges (reference fno.py:330, :337, :449, :458) ---------------
     def x_to_ky(self, comm: Communicator, label: str) -> torch.Tensor:

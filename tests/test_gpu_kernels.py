@@ -90,8 +90,9 @@ def test_yzt_inverse(grid, modes, dtype):
 
 @pytest.mark.parametrize("nx,mx,P", [(64, 8, 1), (64, 8, 4), (512, 8, 8), (33, 8, 3), (9, 2, 3)])
 @pytest.mark.parametrize("dtype", [_lib.F32, _lib.F64])
-def test_xspec_forward_backward(nx, mx, P, dtype):
-    c, b = 4, 2
+@pytest.mark.parametrize("variant", ["fused", "workspace"])
+def test_xspec_forward_backward(nx, mx, P, dtype, variant):
+    c, b = 4 if variant == "fused" else 5, 2
     grid, modes = (nx, 16, 16, 16), (mx, 8, 8, 8)
     rdt = torch.float32 if dtype == _lib.F32 else torch.float64
     cdt = torch.complex64 if dtype == _lib.F32 else torch.complex128
@@ -110,7 +111,14 @@ def test_xspec_forward_backward(nx, mx, P, dtype):
     wt = torch.tensor(w, dtype=cdt, device="cuda")
     spec = torch.empty((b, c, rx, kyl, rz, rt), dtype=cdt, device="cuda")
     kout = torch.empty_like(kin)
-    call("dfno_xspec_fwd", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(wt), _lib.ptr(spec), _lib.ptr(kout), None)
+    ws = ctypes.c_int64()
+    call("dfno_xspec_workspace", ctypes.byref(g), ctypes.byref(ws))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    if variant == "fused":
+        call("dfno_xspec_fwd", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(wt), _lib.ptr(spec), _lib.ptr(kout), None)
+    else:
+        call("dfno_xspec_fwd_ws", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(wt), _lib.ptr(spec), _lib.ptr(kout),
+             _lib.ptr(work), None)
     kx = O.keep(nx, mx)
     s_ref = np.fft.fft(z, axis=2)[:, :, kx]
     y = np.einsum("bi...,io...->bo...", s_ref, w)
@@ -123,8 +131,12 @@ def test_xspec_forward_backward(nx, mx, P, dtype):
     assert O.rel_err(kout.cpu().numpy(), u_packed) < t
     # backward
     gw = torch.empty_like(wt)
-    call("dfno_xspec_bwd", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(spec), _lib.ptr(wt), _lib.ptr(gw), _lib.ptr(kout),
-         None)
+    if variant == "fused":
+        call("dfno_xspec_bwd", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(spec), _lib.ptr(wt), _lib.ptr(gw),
+             _lib.ptr(kout), None)
+    else:
+        call("dfno_xspec_bwd_ws", ctypes.byref(g), _lib.ptr(kin), _lib.ptr(spec), _lib.ptr(wt), _lib.ptr(gw),
+             _lib.ptr(kout), _lib.ptr(work), None)
     d = np.fft.fft(z, axis=2)[:, :, kx] / nx
     gw_ref = np.einsum("bi...,bo...->io...", np.conj(spec.cpu().numpy().astype(complex)), d)
     dx = np.einsum("bo...,io...->bi...", d, np.conj(w))
