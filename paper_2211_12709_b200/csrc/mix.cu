@@ -424,6 +424,8 @@ static int mix_bwd_dispatch(long long npts, int nb, int cin, int cout, const voi
 
 int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre, const void* src,
                int src_act, int act, const void* w, void* gin, void* partials, int blocks, cudaStream_t st);
+int mix_fwd_tc(long long npts, int nb, int cin, int cout, const void* src, int src_act, int act, const void* w,
+               void* pre, void* post, cudaStream_t st);
 
 static bool mix_tc_enabled() {
   static int v = -1;
@@ -444,8 +446,13 @@ extern "C" int dfno_mix_fwd(const dfno_geom* g, int64_t npts, int cin, int cout,
   if (npts < 0 || cin < 1 || cout < 1) return DFNO_ERR_DIMENSION;
   if (npts == 0 || g->batch == 0) return DFNO_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g->dtype == DFNO_F32)
+  if (g->dtype == DFNO_F32) {
+    if (mix_tc_enabled()) {
+      const int rc = mix_fwd_tc(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
+      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+    }
     return mix_fwd_dispatch<float>(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
+  }
   if (g->dtype == DFNO_F64)
     return mix_fwd_dispatch<double>(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
   return DFNO_ERR_DTYPE;

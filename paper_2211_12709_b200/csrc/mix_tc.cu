@@ -282,4 +282,174 @@ int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, cons
 #undef DFNO_MB
 }
 
+// ===========================================================================
+// forward: pre[b][o][p] = sum_i f(src[b][i][p]) W[i][o]  (post = act(pre))
+// reference _mix_layer_forward d/fno.py:286-289 -> einsum_channel_mix
+// d/tensor.py:210-228, activation d/fno.py:41-46.  One thread per point of a
+// 128-point tile: A = f(src) (128 points x K = i) in TMEM, B = W^T (o x i) in
+// shared memory, D (points x o) read back by the owning thread.  Up to four
+// CTAs per SM; the MMAs of tile t run while tile t + 1 is loaded.
+// ===========================================================================
+namespace {
+constexpr uint32_t kMfTmemCols = 128;  // D 0..31 | A hi 32..63 | A lo 64..95
+}
+
+template <int CM, bool EXACT, int ACT>
+__global__ void __launch_bounds__(kMbThreads, 4) k_mix_fwd_tc(long long npts, int nb, int cin_rt, int cout_rt,
+                                                              const float* __restrict__ src, int src_act,
+                                                              const float* __restrict__ w, float* __restrict__ pre,
+                                                              float* __restrict__ post) {
+  const int cin = EXACT ? CM : cin_rt, cout = EXACT ? CM : cout_rt;
+  __shared__ __align__(1024) unsigned char b1[2 * 4096];  // W^T hi plane, lo plane (N = o <= 32, K = i <= 32)
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int KPi = (cin + 7) & ~7;    // K (i)
+  const int NPo = (cout + 15) & ~15; // N (o)
+  const int sbo = (KPi / 4) * 128;
+  const int plane = (NPo / 8) * sbo;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < NPo * KPi; e += kMbThreads) {
+    const int o = e / KPi, i = e % KPi;
+    const float v = (i < cin && o < cout) ? w[(long long)i * cout + o] : 0.f;
+    float h, l;
+    tc::split_rn(v, h, l);
+    const int off = (o >> 3) * sbo + (i >> 2) * 128 + (o & 7) * 16 + (i & 3) * 4;
+    *reinterpret_cast<float*>(b1 + off) = h;
+    *reinterpret_cast<float*>(b1 + plane + off) = l;
+  }
+  if (warp == 0) tc::tmem_alloc<kMfTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t d = tmem, ah = tmem + 32, al = tmem + 64;
+  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+  const long long tiles_per_b = (npts + kMbThreads - 1) / kMbThreads;
+  const long long ntiles = tiles_per_b * nb;
+
+  float sv[CM];
+  auto load = [&](long long tile) {
+    const long long bb = tile / tiles_per_b;
+    const long long p = (tile - bb * tiles_per_b) * kMbThreads + tid;
+    const bool valid = tile < ntiles && p < npts;
+    const float* s0 = src + (bb * cin) * npts + p;
+#pragma unroll
+    for (int i = 0; i < CM; ++i) {
+      sv[i] = (valid && (EXACT || i < cin)) ? __ldcs(s0) : 0.f;
+      s0 += npts;
+    }
+  };
+  long long prev_out = -1;
+  auto drain = [&]() {
+    uint32_t r[32];
+    tc::tmem_ld32_nowait(d + lane_off, r);
+    tc::tmem_ld_wait();
+    if (prev_out >= 0) {
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        if (EXACT || o < cout) {
+          const float v = __uint_as_float(r[o]);
+          __stcs(pre + prev_out + (long long)o * npts, v);
+          if (post) __stcs(post + prev_out + (long long)o * npts, act_apply<float>(ACT, v));
+        }
+      }
+    }
+  };
+  int it = 0;
+  load(blockIdx.x);
+#pragma unroll 1
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const long long bb = tile / tiles_per_b;
+    const long long p = (tile - bb * tiles_per_b) * kMbThreads + tid;
+    float h[32], l[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < CM) tc::split_hl(src_act ? act_apply<float>(ACT, sv[i]) : sv[i], h[i], l[i]);
+      else h[i] = l[i] = 0.f;
+    }
+    load(tile + gridDim.x);
+    if (it > 0) {
+      tc::mbar_wait(&bar, (it - 1) & 1);
+      tc::fence_after();
+      drain();
+    }
+    tc::tmem_st32(ah + lane_off, h);
+    tc::tmem_st32(al + lane_off, l);
+    tc::tmem_st_wait();
+    tc::fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t id = tc::idesc_tf32(128, NPo);
+      const uint32_t sb = tc::smem_u32(b1);
+      for (int s = 0; s < KPi / 8; ++s) {
+        const uint64_t bh = tc::desc(sb + s * 256, 128, sbo), bl = tc::desc(sb + plane + s * 256, 128, sbo);
+        tc::mma_tf32_ts(d, ah + 8 * s, bh, id, s > 0 ? 1u : 0u);
+        tc::mma_tf32_ts(d, al + 8 * s, bh, id, 1u);
+        tc::mma_tf32_ts(d, ah + 8 * s, bl, id, 1u);
+      }
+      tc::commit(&bar);
+    }
+    prev_out = (p < npts) ? (bb * cout * npts + p) : -1;
+  }
+  if (it > 0) {
+    tc::mbar_wait(&bar, (it - 1) & 1);
+    tc::fence_after();
+    drain();
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kMfTmemCols>(tmem);
+}
+
+template <int CM, bool EXACT, int ACT>
+static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const void* src, int src_act, const void* w,
+                              void* pre, void* post, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long tiles = ((npts + kMbThreads - 1) / kMbThreads) * nb;
+  const long long blocks = tiles < 4LL * sms ? tiles : 4LL * sms;
+  k_mix_fwd_tc<CM, EXACT, ACT><<<(unsigned)blocks, kMbThreads, 0, st>>>(npts, nb, cin, cout, (const float*)src, src_act,
+                                                                        (const float*)w, (float*)pre, (float*)post);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+template <int CM, bool EXACT>
+static int launch_mix_fwd_tc(long long npts, int nb, int cin, int cout, const void* src, int src_act, int act,
+                             const void* w, void* pre, void* post, cudaStream_t st) {
+  switch (act) {
+    case DFNO_ACT_GELU:
+      return launch_mix_fwd_tc3<CM, EXACT, DFNO_ACT_GELU>(npts, nb, cin, cout, src, src_act, w, pre, post, st);
+    case DFNO_ACT_RELU:
+      return launch_mix_fwd_tc3<CM, EXACT, DFNO_ACT_RELU>(npts, nb, cin, cout, src, src_act, w, pre, post, st);
+    default:
+      return launch_mix_fwd_tc3<CM, EXACT, DFNO_ACT_IDENTITY>(npts, nb, cin, cout, src, src_act, w, pre, post, st);
+  }
+}
+
+// fp32, cin and cout <= 32; returns DFNO_ERR_UNSUPPORTED otherwise.
+int mix_fwd_tc(long long npts, int nb, int cin, int cout, const void* src, int src_act, int act, const void* w,
+               void* pre, void* post, cudaStream_t st) {
+  const int m = cin > cout ? cin : cout;
+  if (m > 32 || npts < 1) return DFNO_ERR_UNSUPPORTED;
+#define DFNO_MF(CM, EX) return launch_mix_fwd_tc<CM, EX>(npts, nb, cin, cout, src, src_act, act, w, pre, post, st)
+  if (cin == 20 && cout == 20) DFNO_MF(20, true);
+  if (m <= 8) DFNO_MF(8, false);
+  if (m <= 16) DFNO_MF(16, false);
+  if (m <= 24) DFNO_MF(24, false);
+  DFNO_MF(32, false);
+#undef DFNO_MF
+}
+
 }  // namespace dfno

@@ -32,7 +32,14 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     k = ctypes.c_int()
     lib.dfno_mix_bwd_partials(gp, npts, c, c, ctypes.byref(n), ctypes.byref(k))
     parts = torch.empty(n.value, device="cuda")
+    ws = ctypes.c_int64()
+    lib.dfno_xspec_workspace(gp, ctypes.byref(ws))
+    work = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
     fns = {
+        "xspec_fwd_ws": lambda: lib.dfno_xspec_fwd_ws(gp, _lib.ptr(xk), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(out),
+                                                      _lib.ptr(work), st),
+        "xspec_bwd_ws": lambda: lib.dfno_xspec_bwd_ws(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(w),
+                                                      _lib.ptr(out), _lib.ptr(work), st),
         "yzt_fwd": lambda: lib.dfno_dft_yzt_fwd(gp, _lib.ptr(a), None, _lib.SRC_ACT, 1.0, _lib.ptr(xk), st),
         "yzt_fwd_grad": lambda: lib.dfno_dft_yzt_fwd(gp, _lib.ptr(a), _lib.ptr(p), _lib.SRC_GRAD, 1.0, _lib.ptr(xk), st),
         "yzt_inv": lambda: lib.dfno_dft_yzt_inv(gp, _lib.ptr(xk), 1.0, _lib.ptr(b), st),
