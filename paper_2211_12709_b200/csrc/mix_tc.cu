@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
                                                               float* __restrict__ partials) {
   const int cin = EXACT ? CM : cin_rt, cout = EXACT ? CM : cout_rt;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;  // GEMM1 (input grad, thread 0) / GEMM2 (weight grad, thread 32) commits
   __shared__ uint32_t tmem_base;
   unsigned char* a2 = smem;
   unsigned char* b2 = smem + kMbOpBytes;
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   if (warp == 0) tc::tmem_alloc<kMbTmemCols>(&tmem_base);
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
+    tc::mbar_init(&bar2, 1);
     tc::mbar_fence_init();
   }
   tc::fence_proxy_async();
@@ -143,7 +144,8 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     }
     load(tile + gridDim.x);
     if (it > 0) {  // MMAs of the previous tile done: its operands are free, D1 holds its input grad
-      tc::mbar_wait(&bar, (it - 1) & 1);
+      if (want_gin) tc::mbar_wait(&bar, (it - 1) & 1);
+      tc::mbar_wait(&bar2, (it - 1) & 1);
       tc::fence_after();
       if (want_gin) drain_gin();
     }
@@ -179,31 +181,34 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     tc::fence_proxy_async();
     tc::fence_before();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && want_gin) {
       tc::fence_after();
-      if (want_gin) {
-        const uint32_t id1 = tc::idesc_tf32(128, NPi);
-        const uint32_t sb1 = tc::smem_u32(b1);
-        for (int s = 0; s < KPo / 8; ++s) {
-          const uint64_t bh = tc::desc(sb1 + s * 256, 128, sbo_b1);
-          const uint64_t bl = tc::desc(sb1 + b1_plane + s * 256, 128, sbo_b1);
-          tc::mma_tf32_ts(d1, a1h + 8 * s, bh, id1, s > 0 ? 1u : 0u);
-          tc::mma_tf32_ts(d1, a1l + 8 * s, bh, id1, 1u);
-          tc::mma_tf32_ts(d1, a1h + 8 * s, bl, id1, 1u);
-        }
+      const uint32_t id1 = tc::idesc_tf32(128, NPi);
+      const uint32_t sb1 = tc::smem_u32(b1);
+      for (int s = 0; s < KPo / 8; ++s) {
+        const uint64_t bh = tc::desc(sb1 + s * 256, 128, sbo_b1);
+        const uint64_t bl = tc::desc(sb1 + b1_plane + s * 256, 128, sbo_b1);
+        tc::mma_tf32_ts(d1, a1h + 8 * s, bh, id1, s > 0 ? 1u : 0u);
+        tc::mma_tf32_ts(d1, a1l + 8 * s, bh, id1, 1u);
+        tc::mma_tf32_ts(d1, a1h + 8 * s, bl, id1, 1u);
       }
+      tc::commit(&bar);
+    }
+    if (tid == 32) {  // second issuing warp: the weight-gradient GEMM overlaps GEMM1's issue
+      tc::fence_after();
       const uint32_t id2 = tc::idesc_tf32(128, 64);
       const uint32_t sa2 = tc::smem_u32(a2), sb2 = tc::smem_u32(b2);
 #pragma unroll 4
       for (int s = 0; s < kMbThreads / 8; ++s)
         tc::mma_tf32(d2, tc::desc(sa2 + s * 2 * kMbLbo, kMbLbo, kMbSbo), tc::desc(sb2 + s * 2 * kMbLbo, kMbLbo, kMbSbo),
                      id2, (it > 0 || s > 0) ? 1u : 0u);
-      tc::commit(&bar);
+      tc::commit(&bar2);
     }
     prev_out = valid ? (bb * cin * npts + p) : -1;
   }
   if (it > 0) {
-    tc::mbar_wait(&bar, (it - 1) & 1);
+    if (want_gin) tc::mbar_wait(&bar, (it - 1) & 1);
+    tc::mbar_wait(&bar2, (it - 1) & 1);
     tc::fence_after();
     if (want_gin) drain_gin();
   }
