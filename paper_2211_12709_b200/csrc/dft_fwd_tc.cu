@@ -388,10 +388,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
     if (lane == 0) {
       tc::tma_prefetch_desc(&tm_src);
       if (GRAD) tc::tma_prefetch_desc(&tm_pre);
-      GroupIdx gi;
-      int tb = 0;
-      for (int i = 0; i < n_tiles; ++i) {
-        const int s = i % S, n = i / S;
+      GroupIdx gi, gp;  // gp runs kPf tiles ahead: L2 prefetch deepens the stream beyond the smem ring
+      int tb = 0, tbp = 0;
+      constexpr int kPf = 6;
+      for (int i = 0; i < n_tiles + kPf; ++i) {
+        if (i < n_tiles) {
+          const int slabp = (int)blockIdx.x + gp.slab_g * (int)gridDim.x;
+          tc::tma_prefetch_4d(&tm_src, tbp * 32, gp.zb * 16, gp.yc * 8, slabp);
+          if (GRAD) tc::tma_prefetch_4d(&tm_pre, tbp * 32, gp.zb * 16, gp.yc * 8, slabp);
+          if (++tbp == L.ntb) {
+            tbp = 0;
+            gp.next(L);
+          }
+        }
+        if (i < kPf) continue;
+        const int j = i - kPf;
+        const int s = j % S, n = j / S;
         const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
         DFNO_W(0, tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64));
         tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
