@@ -41,18 +41,22 @@ __device__ void fill_tw(float2* tw, const dfno_geom& g) {
 }
 }  // namespace
 
-// one thread per (b, c, m) column; RXM >= rx register accumulators
-template <int RXM>
+// one thread per (b, c, m) column and kx share: KS threads split the r_x
+// outputs of a column (RXM each) for parallelism; the shared Z loads hit L1.
+template <int RXM, int KS>
 __global__ void __launch_bounds__(kXT) k_xdft(const dfno_geom g, const float2* __restrict__ kx_in, float s1,
                                               float2* __restrict__ X) {
   extern __shared__ float2 tw[];
   fill_tw(tw, g);
   const long long mloc = mloc_of(g);
-  const long long n = (long long)g.batch * g.c * mloc;
+  const long long n = (long long)g.batch * g.c * mloc * KS;
   const int rx = g.rx;
   for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
-    const long long m = e % mloc, bc = e / mloc;
+    const long long m = e % mloc, q = e / mloc;
+    const int h = (int)(q % KS);
+    const long long bc = q / KS;
     const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
+    const int k0 = h * RXM;
     float2 acc[RXM];
 #pragma unroll
     for (int k = 0; k < RXM; ++k) acc[k] = make_float2(0.f, 0.f);
@@ -61,50 +65,57 @@ __global__ void __launch_bounds__(kXT) k_xdft(const dfno_geom g, const float2* _
       const float2* src = kx_in + kx_row(g, bb, c, x0) + m;
 #pragma unroll 4
       for (int x = x0; x < x1; ++x) {
-        const float2 z = __ldcs(src);
+        const float2 z = __ldg(src);
         src += mloc;
-        const float2* t = tw + x * rx;
+        const float2* t = tw + x * rx + k0;
 #pragma unroll
         for (int k = 0; k < RXM; ++k)
-          if (k < rx) cmac<float>(acc[k], z, t[k]);
+          if (k0 + k < rx) cmac<float>(acc[k], z, t[k]);
       }
     }
-    float2* dst = X + (bc * rx) * mloc + m;
+    float2* dst = X + (bc * rx + k0) * mloc + m;
 #pragma unroll
     for (int k = 0; k < RXM; ++k)
-      if (k < rx) dst[(long long)k * mloc] = make_float2(s1 * acc[k].x, s1 * acc[k].y);
+      if (k0 + k < rx) dst[(long long)k * mloc] = make_float2(s1 * acc[k].x, s1 * acc[k].y);
   }
 }
 
-// one thread per (b, c, m) column: all Nx outputs
-template <int RXM>
+// one thread per (b, c, m) column and x share: XS threads split the Nx
+// outputs of a column for parallelism.
+template <int RXM, int XS>
 __global__ void __launch_bounds__(kXT) k_xidft(const dfno_geom g, const float2* __restrict__ Y, float s2,
                                                float2* __restrict__ kx_out) {
   extern __shared__ float2 tw[];
   fill_tw(tw, g);
   const long long mloc = mloc_of(g);
-  const long long n = (long long)g.batch * g.c * mloc;
-  const int rx = g.rx;
+  const long long n = (long long)g.batch * g.c * mloc * XS;
+  const int rx = g.rx, Nx = g.nx;
   for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
-    const long long m = e % mloc, bc = e / mloc;
+    const long long m = e % mloc, q = e / mloc;
+    const int h = (int)(q % XS);
+    const long long bc = q / XS;
     const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
     float2 yv[RXM];
     const float2* src = Y + (bc * rx) * mloc + m;
 #pragma unroll
     for (int k = 0; k < RXM; ++k) yv[k] = (k < rx) ? src[(long long)k * mloc] : make_float2(0.f, 0.f);
-    for (int p = 0; p < g.nranks; ++p) {
-      const int x0 = g.x_starts[p], x1 = g.x_starts[p + 1];
-      float2* dst = kx_out + kx_row(g, bb, c, x0) + m;
+    const int xa = (int)(((long long)Nx * h) / XS), xb = (int)(((long long)Nx * (h + 1)) / XS);
+    int p = 0;
+    while (xa >= g.x_starts[p + 1]) ++p;
+    float2* dst = kx_out + kx_row(g, bb, c, xa) + m;
 #pragma unroll 2
-      for (int x = x0; x < x1; ++x) {
-        const float2* t = tw + x * rx;
-        float2 a = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < RXM; ++k)
-          if (k < rx) cmac_conj_b<float>(a, yv[k], t[k]);  // e^{+i} = conj(e^{-i})
-        __stcs(dst, make_float2(s2 * a.x, s2 * a.y));
-        dst += mloc;
+    for (int x = xa; x < xb; ++x) {
+      if (x == g.x_starts[p + 1]) {  // next peer chunk of the KX layout
+        ++p;
+        dst = kx_out + kx_row(g, bb, c, x) + m;
       }
+      const float2* t = tw + x * rx;
+      float2 a = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < RXM; ++k)
+        if (k < rx) cmac_conj_b<float>(a, yv[k], t[k]);  // e^{+i} = conj(e^{-i})
+      __stcs(dst, make_float2(s2 * a.x, s2 * a.y));
+      dst += mloc;
     }
   }
 }
@@ -211,8 +222,8 @@ unsigned grid_for(long long n) {
 
 int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
-  const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
-  auto k = g.rx <= 16 ? k_xdft<16> : k_xdft<32>;
+  const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt * 2;
+  auto k = g.rx <= 16 ? k_xdft<8, 2> : k_xdft<16, 2>;
   if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);
@@ -223,7 +234,7 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
 int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
   const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
-  auto k = g.rx <= 16 ? k_xidft<16> : k_xidft<32>;
+  auto k = g.rx <= 16 ? k_xidft<16, 1> : k_xidft<32, 1>;
   if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);

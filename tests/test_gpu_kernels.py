@@ -88,7 +88,7 @@ def test_yzt_inverse(grid, modes, dtype):
     assert O.rel_err(out.cpu().numpy(), want) < tol(dtype)
 
 
-@pytest.mark.parametrize("nx,mx,P", [(64, 8, 1), (64, 8, 4), (512, 8, 8), (33, 8, 3), (9, 2, 3)])
+@pytest.mark.parametrize("nx,mx,P", [(64, 8, 1), (64, 8, 4), (512, 8, 8), (33, 8, 3), (9, 2, 3), (9, 5, 3)])
 @pytest.mark.parametrize("dtype", [_lib.F32, _lib.F64])
 @pytest.mark.parametrize("variant", ["fused", "workspace"])
 def test_xspec_forward_backward(nx, mx, P, dtype, variant):
