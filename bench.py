@@ -300,6 +300,11 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel
     hbm, hbm_kind = peaks()
+    traffic_tbl, traffic_src = {}, None
+    tf = sorted((ROOT / "profiles").glob("*_traffic.json"))
+    if tf:
+        tj = json.loads(tf[-1].read_text())
+        traffic_tbl, traffic_src = tj.get("bytes_per_launch", {}), f"{tf[-1].name}: {tj.get('source', '')}"
     ab = alg_bytes(cfg, xl, kyl, world)
     dom = max(ksum.items(), key=lambda kv: kv[1][1])
     dname, (dn, dms) = dom
@@ -330,7 +335,8 @@ def run_ours(args):
                      "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)" if hbm_kind == "measured" else
                      "fallback (B200_PROFILING.md)",
                      "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "alg_bytes_per_launch": ab[dname], "avg_launch_ms": round(davg, 5), "traffic": None},
+                     "alg_bytes_per_launch": ab[dname], "avg_launch_ms": round(davg, 5),
+                     "traffic": traffic_tbl.get(dname), "traffic_source": traffic_src},
         "step_roofline": {"alg_bytes_per_step_per_gpu": int(step_bytes),
                           "achieved_GBps": round(step_bytes / (ms_max * 1e-3) / 1e9, 1),
                           "frac": round(step_bytes / (ms_max * 1e-3) / 1e9 / hbm, 4)},

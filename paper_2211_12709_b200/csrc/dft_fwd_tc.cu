@@ -56,7 +56,7 @@ constexpr int kIssZ = 23, kIssY = 24;     // stage-Z / stage-Y issuers
 constexpr int kWarps = 25;
 constexpr int kThreads2 = kWarps * 32;
 constexpr int kTileBytes = 128 * 32 * 4;            // 128 rows x 32 t fp32
-constexpr int kScratchWarp = 2 * 2 * 16 * 17 * 4;   // [part][yy][kt][z (+1)]
+constexpr int kScratchWarp = 2 * 16 * 17 * 4;       // [yy][kt][z (+1)], one part (re / im) at a time
 constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
 constexpr int kAYPlane = 16 * 512;                  // 128 rows x K 16, SBO 512 (one hi or lo plane of one tile)
 constexpr int kAYBytes = 4 * kAYPlane;              // 2 tiles x (hi, lo)
@@ -95,7 +95,10 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.off_ring = o;
   const int stage = srcs * kTileBytes;
   int s = (smem_cap - o) / stage;
-  s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);  // even: ring stage s always holds tiles of parity s & 1
+  // two converter sets (activation mode) need an even depth so ring stage s
+  // always holds tiles of parity s & 1; the backward mode runs one set
+  if (srcs == 1) s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);
+  else s = s >= 4 ? 4 : (s >= 2 ? s : 0);
   L.stages = s;
   L.total = o + s * stage;
   return L;
@@ -241,9 +244,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
   if (warp < kConvW) {
     // ======================= converters =======================
+    // activation mode: two sets of 4 warps alternate tiles (the GELU is the
+    // long pole); backward mode is memory bound and runs one set so the ring
+    // depth is not split between sets
+    constexpr int kSets = GRAD ? 1 : 2;
     const int set = warp >> 2, r = 32 * (warp & 3) + lane;  // tile row (y_l, z_l) = TMEM lane
     const int sw = r & 7;
-    for (int i = set; i < n_tiles; i += 2) {
+    for (int i = set; set < kSets && i < n_tiles; i += kSets) {
       const int s = i % S, n = i / S;
       DFNO_W(0, tc::mbar_wait_lazy(&full[s], n & 1, 32));
       const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
@@ -285,23 +292,20 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::tmem_ld_wait();
       tc::fence_before();
       tc::mbar_arrive(&d1_empty[b]);
-#pragma unroll
-      for (int kt = 0; kt < 16; ++kt) {
-        scr[((0 * 2 + yy) * 16 + kt) * 17 + lo16] = __uint_as_float(u[kt]);
-        scr[((1 * 2 + yy) * 16 + kt) * 17 + lo16] = __uint_as_float(u[16 + kt]);
-      }
-      __syncwarp();
       DFNO_W(1, tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1));
       tc::fence_after();
 #pragma unroll
       for (int part = 0; part < 2; ++part) {  // A_Z cols: hi re | hi im | lo re | lo im
+#pragma unroll
+        for (int kt = 0; kt < 16; ++kt) scr[(yy * 16 + kt) * 17 + lo16] = __uint_as_float(u[16 * part + kt]);
+        __syncwarp();
         float h[16], l[16];
 #pragma unroll
-        for (int z = 0; z < 16; ++z) tc::split_hl(scr[((part * 2 + yy) * 16 + lo16) * 17 + z], h[z], l[z]);
+        for (int z = 0; z < 16; ++z) tc::split_hl(scr[(yy * 16 + lo16) * 17 + z], h[z], l[z]);
         tc::tmem_st16(tmem + cAZ + 64 * b + 16 * part + quarter_off, h);
         tc::tmem_st16(tmem + cAZ + 64 * b + 32 + 16 * part + quarter_off, l);
+        __syncwarp();
       }
-      __syncwarp();
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(&az_full[b]);

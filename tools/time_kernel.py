@@ -23,6 +23,7 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     a = torch.randn((1, c) + grid, device="cuda")
     p = torch.randn((1, c) + grid, device="cuda")
     b = torch.empty_like(a)
+    s3 = torch.randn((1, c) + grid, device="cuda")  # distinct third activation (no aliasing in mix_bwd)
     xk = torch.randn((1, c, grid[0], 16, 16, 16), dtype=torch.complex64, device="cuda")
     w = torch.randn((c, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
     spec = torch.randn((1, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
@@ -47,7 +48,7 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
         "xspec_bwd": lambda: lib.dfno_xspec_bwd(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(w),
                                                 _lib.ptr(out), st),
         "mix_fwd": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), None, st),
-        "mix_bwd": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(a), 1, _lib.ptr(w),
+        "mix_bwd": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(s3), 1, _lib.ptr(w),
                                             _lib.ptr(b), _lib.ptr(parts), st),
     }
     f = fns[which]
