@@ -197,11 +197,20 @@ def run_ours(args):
     from paper_2211_12709_b200 import fno as F
 
     world, rank, local = dist_env()
+    # DFNO_BENCH_SHARE_GPU=1 with DFNO_BENCH_BACKEND=gloo runs every rank on cuda:0 -- a one-GPU
+    # check of the multi-process path (process groups, uneven all-to-all splits); not a timing mode
+    share = os.environ.get("DFNO_BENCH_SHARE_GPU") == "1"
+    backend = os.environ.get("DFNO_BENCH_BACKEND", "nccl")
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        comm = P.Communicator.from_process_group()
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        comm = P.Communicator.from_process_group(device=dev)
     else:
         comm = P.run_ranks(1, lambda c: c)[0]
     grid, wname = workload(world)

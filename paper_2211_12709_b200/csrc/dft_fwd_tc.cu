@@ -95,10 +95,8 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.off_ring = o;
   const int stage = srcs * kTileBytes;
   int s = (smem_cap - o) / stage;
-  // two converter sets (activation mode) need an even depth so ring stage s
-  // always holds tiles of parity s & 1; the backward mode runs one set
-  if (srcs == 1) s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);
-  else s = s >= 4 ? 4 : (s >= 2 ? s : 0);
+  // two converter sets need an even depth: ring stage s always holds tiles of parity s & 1
+  s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);
   L.stages = s;
   L.total = o + s * stage;
   return L;
@@ -244,10 +242,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
   if (warp < kConvW) {
     // ======================= converters =======================
-    // activation mode: two sets of 4 warps alternate tiles (the GELU is the
-    // long pole); backward mode is memory bound and runs one set so the ring
-    // depth is not split between sets
-    constexpr int kSets = GRAD ? 1 : 2;
+    // two sets of 4 warps alternate tiles (measured faster than one set with a
+    // deeper ring in both modes)
+    constexpr int kSets = 2;
     const int set = warp >> 2, r = 32 * (warp & 3) + lane;  // tile row (y_l, z_l) = TMEM lane
     const int sw = r & 7;
     for (int i = set; set < kSets && i < n_tiles; i += kSets) {
