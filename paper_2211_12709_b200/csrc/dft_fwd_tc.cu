@@ -146,7 +146,7 @@ template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
                   const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap,
-                  unsigned long long* __restrict__ prof) {
+                  unsigned long long* __restrict__ prof, int pf_dist) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
   // optional wait profile (debug): per warp, cycles waiting in slots 0..3 and total
   long long wt[4] = {0, 0, 0, 0};
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       if (GRAD) tc::tma_prefetch_desc(&tm_pre);
       GroupIdx gi, gp;  // gp runs kPf tiles ahead: L2 prefetch deepens the stream beyond the smem ring
       int tb = 0, tbp = 0;
-      constexpr int kPf = 6;
+      const int kPf = pf_dist;
       for (int i = 0; i < n_tiles + kPf; ++i) {
         if (i < n_tiles) {
           const int slabp = (int)blockIdx.x + gp.slab_g * (int)gridDim.x;
@@ -567,7 +567,10 @@ int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, 
   static const bool want_prof = getenv("DFNO_WAIT_PROFILE") && getenv("DFNO_WAIT_PROFILE")[0] == '1';
   if (want_prof && !prof) cudaMalloc(&prof, kWarps * 5 * sizeof(unsigned long long));
   if (prof) cudaMemsetAsync(prof, 0, kWarps * 5 * sizeof(unsigned long long), st);
-  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap, prof);
+  // L2 prefetch distance in tiles (DFNO_YZT_PF overrides, for sweeps)
+  static const int pf_env = getenv("DFNO_YZT_PF") ? atoi(getenv("DFNO_YZT_PF")) : -1;
+  const int pf = pf_env >= 0 ? pf_env : 0;  // measured: prefetching slows the 2-input backward mode
+  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap, prof, pf);
   DFNO_CUDA_CHECK_LAUNCH();
   if (prof) {  // debug: per-warp wait cycles summed over CTAs
     unsigned long long h[kWarps * 5];
