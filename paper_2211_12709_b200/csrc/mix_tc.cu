@@ -149,32 +149,35 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       tc::fence_after();
       if (want_gin) drain_gin();
     }
-    if (want_gin) {
+    {
+      // gp split once (round-to-nearest hi, exact remainder lo; the tensor
+      // core's truncation of lo costs <= 2^-21 relative) and shared by the
+      // GEMM1 A operand (TMEM) and the GEMM2 B operand (shared memory)
       float h[32], l[32];
 #pragma unroll
       for (int o = 0; o < 32; ++o) {
-        if (o < CM) tc::split_rn(gp[o], h[o], l[o]);
+        if (o < CM) tc::split_hl(gp[o], h[o], l[o]);
         else h[o] = l[o] = 0.f;
       }
-      tc::tmem_st32(a1h + lane_off, h);
-      tc::tmem_st32(a1l + lane_off, l);
+      if (want_gin) {
+        tc::tmem_st32(a1h + lane_off, h);
+        tc::tmem_st32(a1l + lane_off, l);
+      }
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        if (EXACT || o < cout) {
+          *reinterpret_cast<float*>(b2 + mb_off(o, tid)) = h[o];
+          *reinterpret_cast<float*>(b2 + mb_off(32 + o, tid)) = l[o];
+        }
+      }
     }
 #pragma unroll
     for (int i = 0; i < CM; ++i) {
       if (EXACT || i < cin) {
         float h, l;
-        tc::split_rn(a[i], h, l);
+        tc::split_hl(a[i], h, l);
         *reinterpret_cast<float*>(a2 + mb_off(i, tid)) = h;
         *reinterpret_cast<float*>(a2 + mb_off(32 + i, tid)) = l;
-      }
-    }
-#pragma unroll
-    for (int o = 0; o < CM; ++o) {
-      if (EXACT || o < cout) {
-        float h, l;
-        tc::split_rn(gp[o], h, l);
-        *reinterpret_cast<float*>(b2 + mb_off(o, tid)) = h;
-        *reinterpret_cast<float*>(b2 + mb_off(32 + o, tid)) = l;
       }
     }
     if (want_gin) tc::tmem_st_wait();
