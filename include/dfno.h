@@ -187,6 +187,23 @@ int dfno_xspec_bwd_ws(const dfno_geom* g, const void* kx_in, const void* spec,
                       const void* w, void* gw, void* kx_out, void* work,
                       void* stream);
 
+/*
+ * Training step (reference train_step d/training.py:96-133): fused residual /
+ * loss / output gradient, and Adam on the real view of a parameter.
+ *   resid = pred - target; grad_out = grad_scale * resid (grad_out may be
+ *   NULL); sse_out[0] (double) = sum resid^2, reduced in a fixed order over
+ *   dfno_mse_partials() double partials (deterministic).
+ *   Adam (d/training.py:52-74): n real elements, step >= 1, every operation
+ *   rounded to the parameter dtype in the reference's order.
+ */
+int dfno_mse_partials(int64_t n, int* num_partials);
+int dfno_mse_grad(const dfno_geom* g, int64_t n, const void* pred, const void* target,
+                  double grad_scale, void* grad_out, void* partials, void* sse_out,
+                  void* stream);
+int dfno_adam(const dfno_geom* g, int64_t n, void* param, const void* grad, void* m,
+              void* v, double lr, double beta1, double beta2, double eps, int step,
+              void* stream);
+
 #ifdef __cplusplus
 }
 #endif

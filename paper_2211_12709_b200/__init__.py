@@ -7,8 +7,9 @@ repartition objects, the collectives with exact accounting, and the labelled
 tensor and spectral helpers -- computed by the sm_100a kernels of
 ``lib/libdfno.so`` (C ABI: include/dfno.h) on CUDA, with NCCL carrying the
 x <-> ky repartitions between GPUs.  Out of scope (not on the FNO path):
-the task pool, training loop / checkpoints, DTNS files, the CLI and the
-socket transport.
+the task pool, checkpoints, DTNS files, the CLI and the
+socket transport.  The training step (train_step, Adam) -- the
+first caller of the path -- runs on device kernels too.
 """
 
 from .comm import (
@@ -30,6 +31,8 @@ from .errors import (
     ExtensionMissingError,
     InfeasiblePartitionError,
     KernelError,
+    NonFiniteLossError,
+    ReplicationError,
     ShapeMismatchError,
     UnknownLabelError,
 )
@@ -55,6 +58,7 @@ from .fno import (
 )
 from .partition import BlockRange, Partition, TransferBlock, block_decompose, range_intersection, repartition_plan
 from .staging import InputStager
+from .training import AdamState, adam_update, global_output_count, train_step
 from .spectral import ModeSpec, fft_dims, ifft_dims, pad_modes, retained_extent, retained_indices, truncate_modes
 from .tensor import (
     DATA_LABELS,

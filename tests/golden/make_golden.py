@@ -155,7 +155,72 @@ def comm_volume_case():
     (OUT / "commvolume_9864_p3.json").write_text(json.dumps(res, indent=1, sort_keys=True))
 
 
+def training_case():
+    """The reference's Adam (d/training.py:52-74) on fixed real32 / complex64
+    inputs over 3 steps, and its train_step (d/training.py:96-133) for 3
+    steps at P = 1 and P = 2 on a small real32 config with a smooth target."""
+    from distfno.training import AdamState, adam_update, train_step
+
+    rng = np.random.default_rng(99)
+    out = {}
+    for name, dt in (("r32", np.float32), ("c64", np.complex64)):
+        shape = (5, 7, 3)
+        p0 = rng.standard_normal(shape)
+        if dt == np.complex64:
+            p0 = p0 + 1j * rng.standard_normal(shape)
+        p0 = p0.astype(dt)
+        out[f"adam_{name}_p0"] = p0
+        st = AdamState()
+        lab = ("c", "co", "kx") if dt == np.complex64 else ("c", "co", "x")
+        p = DenseTensor(lab, p0)
+        for k in range(3):
+            g0 = rng.standard_normal(shape) * 10.0 ** (-k)
+            if dt == np.complex64:
+                g0 = g0 + 1j * rng.standard_normal(shape)
+            g0 = g0.astype(dt)
+            out[f"adam_{name}_g{k}"] = g0
+            st.step += 1
+            p = adam_update(st, "w", p, DenseTensor(lab, g0), 1e-3)
+            out[f"adam_{name}_p{k + 1}"] = p.data.copy()
+    meta = {"lr": 1e-3}
+    grid, modes, c, blocks = (8, 8, 8, 4), (2, 2, 2, 2), 2, 2
+    base = cfg_of(grid, modes, c, blocks, "real32", 1)
+    params = init_params(base, 3)
+    x = rng_input(base, 1, 44)
+    xx = np.linspace(0.0, 1.0, grid[0])[None, None, :, None, None, None]
+    y = (np.sin(2 * np.pi * xx) * np.ones((1, c) + grid)).astype(np.float32)
+    out["train_x"], out["train_y"] = x.data, y
+    for P in (1, 2):
+        cfg = cfg_of(grid, modes, c, blocks, "real32", P)
+        xpart = cfg.x_partition()
+
+        def worker(comm, cfg=cfg, xpart=xpart):
+            lp = shard_params(params, cfg, comm.rank)
+            xl = slice_local(x, xpart, comm.rank)
+            yl = slice_local(DenseTensor(DATA_LABELS, y), xpart, comm.rank)
+            st = AdamState()
+            losses = []
+            for _ in range(3):
+                lp, loss = train_step(comm, xl, yl, lp, st, 1e-3, cfg)
+                losses.append(loss)
+            return losses, lp
+
+        res = run_ranks(P, worker)
+        meta[f"train_losses_p{P}"] = res[0][0]
+        out[f"train_we_p{P}"] = res[0][1].we.data
+        out[f"train_wd_p{P}"] = res[0][1].wd.data
+        for i in range(blocks):
+            out[f"train_w{i}_p{P}"] = np.concatenate([r[1].blocks[i].data for r in res], axis=3)
+    np.savez_compressed(OUT / "training_r32.npz", **out)
+    (OUT / "training_r32.json").write_text(json.dumps(meta, indent=1))
+    print("training", list(out))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "training":
+        training_case()
+        sys.exit(0)
+    training_case()
     partitions()
     init_digests()
     comm_volume_case()
