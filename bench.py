@@ -240,6 +240,20 @@ def run_ours(args):
 
     timer = KernelTimer()
     F.set_kernel_timer(timer)
+    # all-to-all (x <-> ky repartition) time and off-rank bytes, N > 1
+    a2a = {"events": [], "bytes": 0}
+    if world > 1:
+        orig_exchange = comm.exchange
+
+        def timed_exchange(send, recv, send_counts, recv_counts, label=""):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            orig_exchange(send, recv, send_counts, recv_counts, label)
+            e.record()
+            a2a["events"].append((s, e))
+            a2a["bytes"] += sum(n for p, n in enumerate(send_counts) if p != rank) * send.element_size()
+
+        comm.exchange = timed_exchange
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -252,6 +266,15 @@ def run_ours(args):
     barrier()
     clock_info = clocks.stop()
     F.set_kernel_timer(None)
+    a2a_info = None
+    if world > 1:
+        comm.exchange = orig_exchange
+        a2a_ms = sum(s_.elapsed_time(e_) for s_, e_ in a2a["events"]) / args.steps
+        a2a_bytes = a2a["bytes"] / args.steps
+        a2a_info = {"exchanges_per_step": len(a2a["events"]) / args.steps, "ms_per_step": round(a2a_ms, 4),
+                    "off_rank_bytes_per_step": int(a2a_bytes),
+                    "GBps_per_direction": round(a2a_bytes / (a2a_ms * 1e-3) / 1e9, 1) if a2a_ms > 0 else None,
+                    "nvlink_peak_GBps_per_direction": 900.0, "rank": rank}
     ms = t0.elapsed_time(t1) / args.steps
     ms_max = ms
     if world > 1:
@@ -352,6 +375,7 @@ def run_ours(args):
         "kernels": kernels,
         "gpu_launches": int(round(timer.launches)),
         "gpu_launches_per_step": launches_per_step,
+        "all_to_all": a2a_info,
         "clocks": clock_info,
         "e2e": e2e,
     }
