@@ -35,7 +35,8 @@ from .tensor import DATA_LABELS, DenseTensor
 
 
 class InputStager:
-    def __init__(self, shape, dtype=torch.float32, device=None, depth: int = 2, labels=DATA_LABELS):
+    def __init__(self, shape, dtype=torch.float32, device=None, depth: int = 2, labels=DATA_LABELS,
+                 copy_streams: int = 1):
         if depth < 2:
             raise ValueError("depth must be >= 2 (one slot computing, one filling)")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -43,8 +44,10 @@ class InputStager:
         self.dtype = dtype
         self.labels = tuple(labels)
         self.slots = [torch.empty(self.shape, dtype=dtype, device=self.device) for _ in range(depth)]
-        self.copy_stream = torch.cuda.Stream(device=self.device)
-        self.filled = [torch.cuda.Event() for _ in range(depth)]     # H2D of the slot done
+        # the copy may be split over several streams (measured: one is fastest on PCIe Gen5)
+        self.copy_streams = [torch.cuda.Stream(device=self.device) for _ in range(max(1, copy_streams))]
+        self.copy_stream = self.copy_streams[0]
+        self.filled = [[torch.cuda.Event() for _ in self.copy_streams] for _ in range(depth)]  # H2D parts done
         self.released = [None] * depth                               # compute done with the slot
         self.pending = deque()                                       # slots filled, not yet handed out
         self.in_use = None                                           # slot handed out by the last get()
@@ -61,11 +64,15 @@ class InputStager:
         if len(self.pending) + (self.in_use is not None) >= len(self.slots):
             raise RuntimeError("InputStager: every slot is filled or in use; get() before put()")
         self.next_slot = (s + 1) % len(self.slots)
-        with torch.cuda.stream(self.copy_stream):
-            if self.released[s] is not None:
-                self.copy_stream.wait_event(self.released[s])
-            self.slots[s].copy_(data, non_blocking=True)
-            self.filled[s].record(self.copy_stream)
+        src, dst = data.reshape(-1), self.slots[s].reshape(-1)
+        n, k = src.numel(), len(self.copy_streams)
+        for j, cs in enumerate(self.copy_streams):
+            a, b = n * j // k, n * (j + 1) // k
+            with torch.cuda.stream(cs):
+                if self.released[s] is not None:
+                    cs.wait_event(self.released[s])
+                dst[a:b].copy_(src[a:b], non_blocking=True)
+                self.filled[s][j].record(cs)
         self.h2d_bytes += data.numel() * data.element_size()
         self.pending.append(s)
 
@@ -81,9 +88,11 @@ class InputStager:
             ev.record(cur)
             self.released[self.in_use] = ev
         s = self.pending.popleft()
-        cur.wait_event(self.filled[s])
+        for ev in self.filled[s]:
+            cur.wait_event(ev)
         self.in_use = s
         return DenseTensor(self.labels, self.slots[s])
 
     def synchronize(self) -> None:
-        self.copy_stream.synchronize()
+        for cs in self.copy_streams:
+            cs.synchronize()
