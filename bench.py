@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-train", action="store_true")
     p.add_argument("--sample-ranks", type=int, default=16, help="CPU sample: 1/R of the job per process")
     return p.parse_args()
 
@@ -284,6 +285,35 @@ def run_ours(args):
     launches_per_step = timer.launches / args.steps
     ksum = timer.summary()
 
+    # ---- training step: forward, global MSE, backward, Adam,
+    #      replication check -- the reference's train_step (d/training.py:96-133)
+    train = None
+    if not args.no_train:
+        from paper_2211_12709_b200 import training as T
+
+        tgt = P.DenseTensor(P.DATA_LABELS, torch.zeros((1, CHANNELS, xl) + grid[1:], device=dev))
+        st = T.AdamState()
+        tp = params
+        for _ in range(2):
+            tp, _ = T.train_step(comm, x, tgt, tp, st, 1e-4, cfg)
+        barrier()
+        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nt = max(2, min(args.steps, 5))
+        ta.record()
+        for _ in range(nt):
+            tp, tloss = T.train_step(comm, x, tgt, tp, st, 1e-4, cfg)
+        tb.record()
+        barrier()
+        tms = ta.elapsed_time(tb) / nt
+        if world > 1:
+            tt = torch.tensor([tms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tms = float(tt.item())
+        train = {"metric": "train_step samples/s (fwd + MSE + bwd + Adam + replication check)",
+                 "value": round(world * 1e3 / tms, 3), "unit": "samples/s", "ms_per_step": round(tms, 4),
+                 "steps": nt, "loss": tloss}
+        del tp, st
+
     # ---- e2e through the public API with host-resident input
     e2e = None
     if not args.no_e2e:
@@ -378,6 +408,7 @@ def run_ours(args):
         "all_to_all": a2a_info,
         "clocks": clock_info,
         "e2e": e2e,
+        "train_step": train,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cfg.grid, args.sample_ranks * world, steps=1)
