@@ -7,7 +7,7 @@ repartition objects, the collectives with exact accounting, and the labelled
 tensor and spectral helpers -- computed by the sm_100a kernels of
 ``lib/libdfno.so`` (C ABI: include/dfno.h) on CUDA, with NCCL carrying the
 x <-> ky repartitions between GPUs.  Out of scope (not on the FNO path):
-the task pool, checkpoints, DTNS files, the CLI and the
+the task pool, the CLI and the
 socket transport.  The training step (train_step, Adam) -- the
 first caller of the path -- runs on device kernels too.
 """
@@ -31,7 +31,11 @@ from .errors import (
     ExtensionMissingError,
     InfeasiblePartitionError,
     KernelError,
+    MalformedHeaderError,
     NonFiniteLossError,
+    SerializationError,
+    TruncatedPayloadError,
+    UnknownDTypeError,
     ReplicationError,
     ShapeMismatchError,
     UnknownLabelError,
@@ -57,6 +61,7 @@ from .fno import (
     slice_local,
 )
 from .partition import BlockRange, Partition, TransferBlock, block_decompose, range_intersection, repartition_plan
+from .dtns import gather_params, load_checkpoint, save_checkpoint, serialized_size, tensor_from_bytes, tensor_read, tensor_to_bytes, tensor_write
 from .staging import InputStager
 from .training import AdamState, adam_update, global_output_count, train_step
 from .spectral import ModeSpec, fft_dims, ifft_dims, pad_modes, retained_extent, retained_indices, truncate_modes

@@ -449,8 +449,9 @@ class Communicator:
                     raise CollectiveMismatchError(f"gather labels disagree: {labels} vs {t.labels}")
             blocks = [b for _, b in blocks]
         else:
+            # complex payloads travel as their real view (NCCL has no complex type)
             if self.rank != root:
-                self._be.send(data, root)
+                self._be.send(torch.view_as_real(data) if data.is_complex() else data, root)
                 self.stats.record(GATHER, t.size, t.size * t.dtype.itemsize)
                 return None
             blocks = []
@@ -461,7 +462,7 @@ class Communicator:
                 s = list(shape)
                 s[axis] = part.extent_of(src)
                 buf = torch.empty(s, dtype=data.dtype, device=self.device)
-                self._be.recv(buf, src)
+                self._be.recv(torch.view_as_real(buf) if buf.is_complex() else buf, src)
                 blocks.append(buf)
         for src, b in enumerate(blocks):
             if b.shape[axis] != part.extent_of(src):

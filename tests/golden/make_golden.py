@@ -216,11 +216,43 @@ def training_case():
     print("training", list(out))
 
 
+def dtns_case():
+    """The reference's DTNS bytes (d/tensor.py:258-320) for four dtypes and
+    a reference checkpoint directory (d/training.py:176-208)."""
+    import shutil
+
+    from distfno.tensor import tensor_to_bytes
+    from distfno.training import save_checkpoint
+
+    rng = np.random.default_rng(21)
+    out = {}
+    cases = {
+        "r32": (("b", "c", "x", "y", "z", "t"), rng.standard_normal((1, 2, 3, 2, 2, 3)).astype(np.float32)),
+        "r64": (("c", "co"), rng.standard_normal((3, 4))),
+        "c64": (("c", "co", "kx", "ky"), (rng.standard_normal((2, 2, 3, 2)) + 1j * rng.standard_normal(
+            (2, 2, 3, 2))).astype(np.complex64)),
+        "c128": (("kz", "kt"), rng.standard_normal((2, 5)) + 1j * rng.standard_normal((2, 5))),
+    }
+    for k, (labels, data) in cases.items():
+        out[f"{k}_data"] = data
+        out[f"{k}_bytes"] = np.frombuffer(tensor_to_bytes(DenseTensor(labels, data)), dtype=np.uint8)
+    np.savez_compressed(OUT / "dtns_ref.npz", **out)
+    cfg = cfg_of((8, 8, 8, 4), (2, 2, 2, 2), 2, 2, "real32", 2, cin=1, cout=3)
+    d = OUT / "ckpt_ref"
+    shutil.rmtree(d, ignore_errors=True)
+    save_checkpoint(str(d), init_params(cfg, 5), cfg, 5)
+    print("dtns", sorted(out), sorted(p.name for p in d.iterdir()))
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "dtns":
+        dtns_case()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "training":
         training_case()
         sys.exit(0)
     training_case()
+    dtns_case()
     partitions()
     init_digests()
     comm_volume_case()
