@@ -1,0 +1,47 @@
+"""The verification drivers on the device path,
+with the reference's options and bars: SPEC criteria 1-4 (parity 1e-10 in
+real64, adjoints 1e-12, finite-difference gradient 1e-5) and the exact
+communication volume of the reference's own drive_comm_volume run
+(tests/golden/commvolume_9864_p3.json)."""
+
+import json
+
+import pytest
+
+import paper_2211_12709_b200 as P
+from paper_2211_12709_b200 import drivers as D
+
+pytestmark = pytest.mark.gpu
+
+
+def run(driver, opts):
+    return P.run_ranks(opts["workers"], lambda comm: driver(comm, opts))[0]
+
+
+def test_comm_volume_equals_reference_run(golden_dir):
+    want = json.loads((golden_dir / "commvolume_9864_p3.json").read_text())
+    got = run(D.drive_comm_volume, {"grid": [9, 8, 6, 4], "modes": [2, 2, 2, 2], "channels": 2, "blocks": 2,
+                                    "dtype": "real64", "seed": 0, "batch": 2, "activation": "gelu", "workers": 3})
+    assert got == want
+
+
+@pytest.mark.parametrize("dtype,tol", [("real64", 1e-10), ("real32", 1e-5)])
+def test_parity_decomposition_invariance(dtype, tol):
+    res = run(D.drive_parity_forward, {"grid": [16, 16, 16, 8], "modes": [4, 4, 4, 3], "channels": 2, "blocks": 4,
+                                       "dtype": dtype, "seed": 7, "workers": 8})
+    assert res["max_rel_err"] < tol
+    assert res["repart_calls_per_rank"] == 8
+    cfg = D.config_from_opts({"grid": [16, 16, 16, 8], "modes": [4, 4, 4, 3], "channels": 2, "blocks": 4,
+                              "dtype": dtype, "workers": 8})
+    assert res["repart_elements_total"] == P.predicted_block_volume(cfg, 1).per_forward_elements
+
+
+def test_adjoint_identities():
+    res = run(D.drive_adjoint, {"seed": 3, "pairs": 5, "workers": 3})
+    assert res["broadcast_reduce_max_err"] < 1e-12 and res["repartition_max_err"] < 1e-12
+
+
+def test_finite_difference_gradient():
+    res = run(D.drive_gradient, {"grid": [8, 8, 8, 4], "modes": [2, 2, 2, 2], "channels": 2, "blocks": 2,
+                                 "dtype": "real64", "seed": 11, "directions": 5, "workers": 2})
+    assert res["max_rel_err"] < 1e-5, res["errors"]
