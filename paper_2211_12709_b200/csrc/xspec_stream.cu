@@ -214,9 +214,9 @@ int sms_x() {
   return n;
 }
 
-unsigned grid_for(long long n) {
+unsigned grid_for(long long n, int per_sm = 8) {
   long long b = (n + kXT - 1) / kXT;
-  const long long cap = (long long)sms_x() * 8;
+  const long long cap = (long long)sms_x() * per_sm;
   return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
@@ -226,7 +226,7 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
   auto k = g.rx <= 16 ? k_xdft<8, 2> : k_xdft<16, 2>;
   if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
-  k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);
+  k<<<grid_for(n, 4), kXT, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);  // fewer CTAs: twiddle setup amortised
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }
@@ -237,7 +237,7 @@ int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaS
   auto k = g.rx <= 16 ? k_xidft<16, 1> : k_xidft<32, 1>;
   if (smem > 48 * 1024 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
-  k<<<grid_for(n), kXT, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);
+  k<<<grid_for(n, 4), kXT, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }

@@ -28,6 +28,7 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     w = torch.randn((c, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
     spec = torch.randn((1, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
     out = torch.empty_like(xk)
+    gw = torch.empty_like(w)
     npts = grid[0] * grid[1] * grid[2] * grid[3]
     n = ctypes.c_int64()
     k = ctypes.c_int()
@@ -39,13 +40,13 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     fns = {
         "xspec_fwd_ws": lambda: lib.dfno_xspec_fwd_ws(gp, _lib.ptr(xk), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(out),
                                                       _lib.ptr(work), st),
-        "xspec_bwd_ws": lambda: lib.dfno_xspec_bwd_ws(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(w),
+        "xspec_bwd_ws": lambda: lib.dfno_xspec_bwd_ws(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw),
                                                       _lib.ptr(out), _lib.ptr(work), st),
         "yzt_fwd": lambda: lib.dfno_dft_yzt_fwd(gp, _lib.ptr(a), None, _lib.SRC_ACT, 1.0, _lib.ptr(xk), st),
         "yzt_fwd_grad": lambda: lib.dfno_dft_yzt_fwd(gp, _lib.ptr(a), _lib.ptr(p), _lib.SRC_GRAD, 1.0, _lib.ptr(xk), st),
         "yzt_inv": lambda: lib.dfno_dft_yzt_inv(gp, _lib.ptr(xk), 1.0, _lib.ptr(b), st),
         "xspec_fwd": lambda: lib.dfno_xspec_fwd(gp, _lib.ptr(xk), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(out), st),
-        "xspec_bwd": lambda: lib.dfno_xspec_bwd(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(w),
+        "xspec_bwd": lambda: lib.dfno_xspec_bwd(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw),
                                                 _lib.ptr(out), st),
         "mix_fwd": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), None, st),
         "mix_bwd": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(s3), 1, _lib.ptr(w),
