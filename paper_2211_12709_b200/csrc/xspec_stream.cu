@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(kXT) k_xmix_bwd(const dfno_geom g, const float
   }
 }
 
+int xdft_tc(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st);
+int xidft_tc(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st);
+
 namespace {
 int sms_x() {
   static int n = 0;
@@ -221,6 +224,8 @@ unsigned grid_for(long long n, int per_sm = 8) {
 }
 
 int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
+  const int rc = xdft_tc(g, kx_in, s1, X, st);  // tcgen05 path (N_x <= 128, r_x <= 16)
+  if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
   const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt * 2;
   auto k = g.rx <= 16 ? k_xdft<8, 2> : k_xdft<16, 2>;
@@ -232,6 +237,8 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
 }
 
 int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
+  const int rc = xidft_tc(g, Y, s2, kx_out, st);
+  if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
   const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
   auto k = g.rx <= 16 ? k_xidft<16, 1> : k_xidft<32, 1>;
