@@ -25,6 +25,7 @@
 // of tile i run while the CTA loads tile i + 1 (one mbarrier per CTA).
 #include "common.cuh"
 #include "tc.cuh"
+#include "tmap.cuh"
 
 namespace dfno {
 
@@ -415,6 +416,168 @@ __global__ void __launch_bounds__(kMbThreads, 4) k_mix_fwd_tc(long long npts, in
   if (warp == 0) tc::tmem_dealloc<kMfTmemCols>(tmem);
 }
 
+// TMA-in / TMA-out variant of k_mix_fwd_tc.  Warp 4 streams (cin x 128-point)
+// boxes of the input into a shared-memory ring; the four worker warps (thread
+// = point) apply the source activation, split hi/lo and store A into TMEM,
+// thread 0 issues the 3xTF32 MMAs into one of two TMEM accumulators, and the
+// workers drain the OTHER accumulator (the previous tile) into a shared
+// staging box that thread 0 writes back with a TMA tensor store one tile
+// later.  One 128-thread barrier per tile; the MMA overlaps the drain and the
+// next tile's loads, and no thread computes a global address.
+constexpr int kMfMaxStages = 8;
+
+template <int CM, bool EXACT, int ACT>
+__global__ void __launch_bounds__(kMbThreads + 32, 3)
+    k_mix_fwd_tma(long long npts, int nb, int cin_rt, int cout_rt, const __grid_constant__ CUtensorMap tm_src,
+                  const __grid_constant__ CUtensorMap tm_pre, const __grid_constant__ CUtensorMap tm_post, int src_act,
+                  const float* __restrict__ w, int has_post, int nstages) {
+  const int cin = EXACT ? CM : cin_rt, cout = EXACT ? CM : cout_rt;
+  // dynamic: ring[nstages][cin][128] | pre staging[2][cout][128] | post staging[2][cout][128]
+  extern __shared__ __align__(1024) unsigned char dyn[];
+  __shared__ __align__(1024) unsigned char b1[2 * 4096];
+  __shared__ uint64_t bar, full[kMfMaxStages], empty[kMfMaxStages];
+  __shared__ uint32_t tmem_base;
+  const int KPi = (cin + 7) & ~7, NPo = (cout + 15) & ~15;
+  const int sbo = (KPi / 4) * 128, plane = (NPo / 8) * sbo;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < NPo * KPi; e += blockDim.x) {
+    const int o = e / KPi, i = e % KPi;
+    const float v = (i < cin && o < cout) ? w[(long long)i * cout + o] : 0.f;
+    float h, l;
+    tc::split_rn(v, h, l);
+    const int off = (o >> 3) * sbo + (i >> 2) * 128 + (o & 7) * 16 + (i & 3) * 4;
+    *reinterpret_cast<float*>(b1 + off) = h;
+    *reinterpret_cast<float*>(b1 + plane + off) = l;
+  }
+  if (warp == 0) tc::tmem_alloc<kMfTmemCols>(&tmem_base);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    for (int s = 0; s < nstages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], kMbThreads);
+    }
+    tc::mbar_fence_init();
+    tc::tma_prefetch_desc(&tm_src);
+    tc::tma_prefetch_desc(&tm_pre);
+    if (has_post) tc::tma_prefetch_desc(&tm_post);
+  }
+  tc::fence_proxy_async();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  // TMEM: D0 0..31 | A hi 32..63 | A lo 64..95 | D1 96..127
+  const uint32_t tmem = tmem_base, ah = tmem + 32, al = tmem + 64;
+  const long long tiles_per_b = (npts + kMbThreads - 1) / kMbThreads;
+  const long long ntiles = tiles_per_b * nb;
+  const int stage_bytes = cin * kMbThreads * 4, out_bytes = cout * kMbThreads * 4;
+  unsigned char* ring = dyn;
+  float* stage_pre = reinterpret_cast<float*>(dyn + nstages * stage_bytes);
+  float* stage_post = reinterpret_cast<float*>(dyn + nstages * stage_bytes + 2 * out_bytes);
+
+  if (warp == 4) {
+    // ---- TMA producer
+    if ((tid & 31) == 0) {
+      int j = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++j) {
+        const int s = j % nstages, n = j / nstages;
+        tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
+        const long long bb = tile / tiles_per_b;
+        const int p0 = (int)((tile - bb * tiles_per_b) * kMbThreads);
+        tc::mbar_expect_tx(&full[s], stage_bytes);
+        tc::tma_load_2d(ring + s * stage_bytes, &tm_src, p0, (int)(bb * cin), &full[s]);
+      }
+    }
+  } else {
+    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+    auto dcol = [&](int k) { return tmem + ((k & 1) ? 96u : 0u); };
+    // drain accumulator of tile k into staging buffer k&1
+    auto drain = [&](int k) {
+      uint32_t r[32];
+      tc::tmem_ld32_nowait(dcol(k) + lane_off, r);
+      tc::tmem_ld_wait();
+      float* sp = stage_pre + (k & 1) * (out_bytes / 4) + tid;
+      float* sq = stage_post + (k & 1) * (out_bytes / 4) + tid;
+#pragma unroll
+      for (int o = 0; o < CM; ++o) {
+        if (EXACT || o < cout) {
+          const float v = __uint_as_float(r[o]);
+          sp[o * kMbThreads] = v;
+          if (has_post) sq[o * kMbThreads] = act_apply<float>(ACT, v);
+        }
+      }
+      tc::fence_proxy_async();
+    };
+    // TMA store of staged tile k (thread 0 only)
+    auto store = [&](int k) {
+      const long long tile = blockIdx.x + (long long)k * gridDim.x;
+      const long long bb = tile / tiles_per_b;
+      const int p0 = (int)((tile - bb * tiles_per_b) * kMbThreads), r0 = (int)(bb * cout);
+      tc::tma_store_2d(&tm_pre, stage_pre + (k & 1) * (out_bytes / 4), p0, r0);
+      if (has_post) tc::tma_store_2d(&tm_post, stage_post + (k & 1) * (out_bytes / 4), p0, r0);
+      tc::bulk_commit();
+    };
+    int it = 0;
+#pragma unroll 1
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int s = it % nstages, n = it / nstages;
+      tc::mbar_wait(&full[s], n & 1);
+      const float* row = reinterpret_cast<const float*>(ring + s * stage_bytes) + tid;
+      float h[32], l[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i < CM && (EXACT || i < cin)) {
+          const float v = row[i * kMbThreads];
+          tc::split_hl(src_act ? act_apply<float>(ACT, v) : v, h[i], l[i]);
+        } else {
+          h[i] = l[i] = 0.f;
+        }
+      }
+      tc::mbar_arrive(&empty[s]);
+      if (it > 0) {
+        tc::mbar_wait(&bar, (it - 1) & 1);  // MMA it-1 done: A free, D(it-1) complete
+        tc::fence_after();
+      }
+      tc::tmem_st32(ah + lane_off, h);
+      tc::tmem_st32(al + lane_off, l);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      if (tid == 0) tc::bulk_wait_read0();  // store of tile it-3 has left staging buffer (it-1)&1
+      tc::named_sync(1, kMbThreads);
+      if (tid == 0) {
+        tc::fence_after();
+        const uint32_t id = tc::idesc_tf32(128, NPo);
+        const uint32_t sb = tc::smem_u32(b1);
+        const uint32_t d = dcol(it);
+        for (int k = 0; k < KPi / 8; ++k) {
+          const uint64_t bh = tc::desc(sb + k * 256, 128, sbo), bl = tc::desc(sb + plane + k * 256, 128, sbo);
+          tc::mma_tf32_ts(d, ah + 8 * k, bh, id, k > 0 ? 1u : 0u);
+          tc::mma_tf32_ts(d, al + 8 * k, bh, id, 1u);
+          tc::mma_tf32_ts(d, ah + 8 * k, bl, id, 1u);
+        }
+        tc::commit(&bar);
+        if (it >= 2) store(it - 2);  // staged by every worker before the barrier above
+      }
+      if (it > 0) drain(it - 1);
+    }
+    if (it > 0) {
+      tc::mbar_wait(&bar, (it - 1) & 1);
+      tc::fence_after();
+      if (tid == 0) tc::bulk_wait_read0();
+      tc::named_sync(1, kMbThreads);
+      if (tid == 0 && it >= 2) store(it - 2);
+      drain(it - 1);
+      tc::named_sync(1, kMbThreads);
+      if (tid == 0) {
+        store(it - 1);
+        tc::bulk_wait0();
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<kMfTmemCols>(tmem);
+}
+
 template <int CM, bool EXACT, int ACT>
 static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const void* src, int src_act, const void* w,
                               void* pre, void* post, cudaStream_t st) {
@@ -426,6 +589,38 @@ static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const v
     if (sms <= 0) sms = 148;
   }
   const long long tiles = ((npts + kMbThreads - 1) / kMbThreads) * nb;
+  static const bool use_tma = [] {
+    const char* e = getenv("DFNO_MF_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  CUtensorMap tm_src, tm_pre, tm_post;
+  if (use_tma && make_rows_map(&tm_src, src, npts, (long long)nb * cin, cin) &&
+      make_rows_map(&tm_pre, pre, npts, (long long)nb * cout, cout) &&
+      (!post || make_rows_map(&tm_post, post, npts, (long long)nb * cout, cout))) {
+    if (!post) tm_post = tm_pre;
+    // per-CTA dynamic shared memory: ring + double-buffered output staging;
+    // 3 CTAs per SM when a ring of >= 2 stages fits, else 2
+    const int stage_bytes = cin * kMbThreads * 4, out_bytes = cout * kMbThreads * 4 * 2 * (post ? 2 : 1);
+    const int static_bytes = 2 * 4096 + 256;
+    int per_sm = 3, stages = 0;
+    for (; per_sm >= 1; --per_sm) {
+      const int avail = (227 * 1024) / per_sm - 1024 - static_bytes - out_bytes;
+      stages = avail / stage_bytes;
+      if (stages >= 2) break;
+    }
+    if (stages > 4) stages = 4;
+    if (per_sm >= 1 && stages >= 2) {
+      const int smem = stages * stage_bytes + out_bytes;
+      auto kt = k_mix_fwd_tma<CM, EXACT, ACT>;
+      if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+        const long long grid = tiles < (long long)per_sm * sms ? tiles : (long long)per_sm * sms;
+        kt<<<(unsigned)grid, kMbThreads + 32, smem, st>>>(npts, nb, cin, cout, tm_src, tm_pre, tm_post, src_act,
+                                                          (const float*)w, post ? 1 : 0, stages);
+        DFNO_CUDA_CHECK_LAUNCH();
+        return DFNO_OK;
+      }
+    }
+  }
   const long long blocks = tiles < 4LL * sms ? tiles : 4LL * sms;
   k_mix_fwd_tc<CM, EXACT, ACT><<<(unsigned)blocks, kMbThreads, 0, st>>>(npts, nb, cin, cout, (const float*)src, src_act,
                                                                         (const float*)w, (float*)pre, (float*)post);

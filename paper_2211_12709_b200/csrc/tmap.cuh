@@ -38,4 +38,18 @@ inline bool make_slab_map(CUtensorMap* m, const void* base, int ny, int nz, int 
          CUDA_SUCCESS;
 }
 
+// 2-D fp32 map over (point, row) of a (rows, npts) tensor, box (128, box_rows),
+// no swizzle: rows of a channel-major activation viewed as (b * c, points).
+inline bool make_rows_map(CUtensorMap* m, const void* base, long long npts, long long rows, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc || (npts * 4) % 16 != 0 || ((uintptr_t)base & 15) || box_rows > 256) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)npts, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)npts * 4};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace dfno

@@ -1,6 +1,7 @@
 """Time one libdfno kernel at the C2 geometry with CUDA events (median of N).
 Usage: python tools/time_kernel.py yzt_fwd|yzt_fwd_grad|yzt_inv|xspec_fwd|xspec_bwd|mix_fwd|mix_bwd [reps]"""
 import ctypes
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -16,7 +17,8 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     lib = _lib.load()
     ret = tuple(min(16, n) for n in grid)
     g = _lib.make_geom(batch=1, c_in=c, c=c, c_out=c, grid=grid, modes=(8, 8, 8, 8), retained=ret, nranks=1,
-                       rank=0, dtype=_lib.F32, act=_lib.ACT_GELU, x_starts=block_starts(grid[0], 1),
+                       rank=0, dtype=_lib.F32,
+                       act=_lib.ACT_IDENTITY if os.environ.get("TK_ACT") == "id" else _lib.ACT_GELU, x_starts=block_starts(grid[0], 1),
                        ky_starts=block_starts(ret[1], 1))
     gp = ctypes.byref(g)
     st = _lib.stream_handle()
@@ -49,6 +51,8 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
         "xspec_bwd": lambda: lib.dfno_xspec_bwd(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw),
                                                 _lib.ptr(out), st),
         "mix_fwd": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), None, st),
+        "mix_fwd_post": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 0, _lib.ptr(w), _lib.ptr(p), _lib.ptr(b),
+                                                 st),
         "mix_bwd": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(s3), 1, _lib.ptr(w),
                                             _lib.ptr(b), _lib.ptr(parts), st),
     }
