@@ -20,6 +20,7 @@ int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
 // TMEM-operand tcgen05 path (dft_fwd_tc.cu)
 int yzt_fwd_tc2(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
 int yzt_inv_tc2(const dfno_geom&, const void*, double, void*, cudaStream_t);
+int yzt_inv_tc3(const dfno_geom&, const void*, double, void*, cudaStream_t);
 // streamed x-spectral stage (xspec_stream.cu)
 size_t xspec_stream_workspace(const dfno_geom&);
 int xspec_fwd_stream(const dfno_geom&, const void*, const void*, void*, void*, void*, cudaStream_t);
@@ -149,6 +150,11 @@ extern "C" int dfno_dft_yzt_inv(const dfno_geom* g, const void* xk_in, double sc
   if (g->dtype == DFNO_F32) {
     if (tc_enabled()) {
       static const bool v1 = env_flag("DFNO_YZT_V1");
+      static const bool inv2 = env_flag("DFNO_INV_V2");
+      if (!v1 && !inv2) {
+        rc = yzt_inv_tc3(*g, xk_in, scale, out, st);
+        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
+      }
       if (!v1) {
         rc = yzt_inv_tc2(*g, xk_in, scale, out, st);
         if (rc != DFNO_ERR_UNSUPPORTED) return rc;

@@ -111,7 +111,16 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 __global__ void __launch_bounds__(kThreadsI, 1)
     k_yzt_inv_tc2(const dfno_geom g, const float2* __restrict__ in, const __grid_constant__ CUtensorMap tm_out,
-                  float scale) {
+                  float scale, unsigned long long* __restrict__ prof) {
+  // optional wait profile (debug, DFNO_WAIT_PROFILE=1): per warp, cycles in wait slots 0..3 and total
+  long long wt[4] = {0, 0, 0, 0};
+  const long long t_start = clock64();
+#define DFNO_W(slot, call)                \
+  do {                                    \
+    const long long t0_ = clock64();      \
+    call;                                 \
+    if (prof) wt[slot] += clock64() - t0_; \
+  } while (0)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t ay_full, ay_empty, dy_full, dy_empty, az_full[2], az_empty[2];
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(kThreadsI, 1)
     for (int si = 0; si < my_slabs; ++si) {
       const int slab = (int)blockIdx.x + si * (int)gridDim.x;
       const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
-      tc::mbar_wait_lazy(&ay_empty, (si & 1) ^ 1, 64);
+      DFNO_W(0, tc::mbar_wait_lazy(&ay_empty, (si & 1) ^ 1, 64));
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         const int kz = 8 * hh + (row >> 4), kt = row & 15;
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       tc::fence_proxy_async();
       tc::mbar_arrive(&ay_full);
       for (int p = 0; p < L.npass; ++p, ++pass_i) {
-        tc::mbar_wait(&dy_full, pass_i & 1);
+        DFNO_W(1, tc::mbar_wait(&dy_full, pass_i & 1));
         tc::fence_after();
         const int nchunk = min(4, L.nyc - 4 * p);
         for (int j = 0; j < nchunk; ++j, ++chunk) {
@@ -251,9 +260,9 @@ __global__ void __launch_bounds__(kThreadsI, 1)
               stash[((1 * 8 + y) * 16 + kt) * 20 + kz] = __uint_as_float(u[2 * hh + 1][y]);
             }
           }
-          tc::named_sync(1, 128);
+          DFNO_W(3, tc::named_sync(1, 128));
           const int b = chunk & 1;
-          tc::mbar_wait(&az_empty[b], ((chunk >> 1) & 1) ^ 1);
+          DFNO_W(2, tc::mbar_wait(&az_empty[b], ((chunk >> 1) & 1) ^ 1));
           tc::fence_after();
           {
             const int yl = 2 * q + yy, kt = lo16;  // A_Z row (y_l, kt)
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(kThreadsI, 1)
           tc::tmem_st_wait();
           tc::fence_before();
           tc::mbar_arrive(&az_full[b]);
-          tc::named_sync(1, 128);  // stash consumed
+          DFNO_W(3, tc::named_sync(1, 128));  // stash consumed
         }
       }
     }
@@ -288,14 +297,14 @@ __global__ void __launch_bounds__(kThreadsI, 1)
     int n = 0;
     for (int c = 0; c < n_chunks; ++c) {
       for (int zb = k; zb < L.nzb; zb += 2, ++n) {
-        tc::mbar_wait(&dz_full[k], n & 1);
+        DFNO_W(0, tc::mbar_wait(&dz_full[k], n & 1));
         tc::fence_after();
         uint32_t u[32];
         tc::tmem_ld32_nowait(tmem + iDZ + 32 * k + qoff, u);  // row (y_l, kt): z re 0..15 | z im
         tc::tmem_ld_wait();
         tc::fence_before();
         tc::mbar_arrive(&dz_empty[k]);
-        tc::mbar_wait(&at_empty[k], (n & 1) ^ 1);
+        DFNO_W(1, tc::mbar_wait(&at_empty[k], (n & 1) ^ 1));
         tc::fence_after();
 #pragma unroll
         for (int part = 0; part < 2; ++part) {  // A_T row (y_l, z_l): kt re | kt im ; hi 0..31, lo 32..63
@@ -332,15 +341,14 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       const int slab = (int)blockIdx.x + si * (int)gridDim.x;
       for (int zb = k; zb < L.nzb; zb += 2) {
         for (int tb = 0; tb < L.ntb; ++tb, ++n) {
-          tc::mbar_wait(&dt_full[k], n & 1);
+          DFNO_W(0, tc::mbar_wait(&dt_full[k], n & 1));
           tc::fence_after();
           uint32_t u[32];
           tc::tmem_ld32_nowait(tmem + iDT + 32 * k + qoff, u);
           tc::tmem_ld_wait();
           tc::fence_before();
           tc::mbar_arrive(&dt_empty[k]);
-          if (leader) bulk_wait_read0();  // previous store has read the staging buffer
-          tc::named_sync(2 + k, 128);
+          DFNO_W(1, if (leader) bulk_wait_read0(); tc::named_sync(2 + k, 128));  // previous store has read the staging buffer
           unsigned char* rowp = stg + r * 128;
 #pragma unroll
           for (int c4 = 0; c4 < 8; ++c4)
@@ -348,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsI, 1)
                 make_float4(scale * __uint_as_float(u[4 * c4]), scale * __uint_as_float(u[4 * c4 + 1]),
                             scale * __uint_as_float(u[4 * c4 + 2]), scale * __uint_as_float(u[4 * c4 + 3]));
           tc::fence_proxy_async();
-          tc::named_sync(2 + k, 128);
+          DFNO_W(2, tc::named_sync(2 + k, 128));
           if (leader) {
             tma_store_4d(&tm_out, stg, tb * 32, zb * 16, yc * 8, slab);
             bulk_commit();
@@ -364,9 +372,9 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       const uint32_t say = tc::smem_u32(ay), sby = tc::smem_u32(by);
       int pass_i = 0;
       for (int si = 0; si < my_slabs; ++si) {
-        tc::mbar_wait_lazy(&ay_full, si & 1, 64);
+        DFNO_W(0, tc::mbar_wait_lazy(&ay_full, si & 1, 64));
         for (int p = 0; p < L.npass; ++p, ++pass_i) {
-          tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1);
+          DFNO_W(1, tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1));
           tc::fence_after();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -397,9 +405,9 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       int n = 0;
       for (int c = 0; c < n_chunks; ++c) {
         const int ab = c & 1;
-        tc::mbar_wait(&az_full[ab], (c >> 1) & 1);
+        DFNO_W(0, tc::mbar_wait(&az_full[ab], (c >> 1) & 1));
         for (int zb = k; zb < L.nzb; zb += 2, ++n) {
-          tc::mbar_wait(&dz_empty[k], (n & 1) ^ 1);
+          DFNO_W(1, tc::mbar_wait(&dz_empty[k], (n & 1) ^ 1));
           tc::fence_after();
           const uint32_t a = tmem + iAZ + 64 * ab, d = tmem + iDZ + 32 * k;
 #pragma unroll
@@ -424,9 +432,9 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       int n = 0, m = 0;
       for (int c = 0; c < n_chunks; ++c) {
         for (int zb = k; zb < L.nzb; zb += 2, ++n) {
-          tc::mbar_wait(&at_full[k], n & 1);
+          DFNO_W(0, tc::mbar_wait(&at_full[k], n & 1));
           for (int tb = 0; tb < L.ntb; ++tb, ++m) {
-            tc::mbar_wait(&dt_empty[k], (m & 1) ^ 1);
+            DFNO_W(1, tc::mbar_wait(&dt_empty[k], (m & 1) ^ 1));
             tc::fence_after();
             const uint32_t a = tmem + iAT + 64 * k, d = tmem + iDT + 32 * k;
 #pragma unroll
@@ -444,6 +452,12 @@ __global__ void __launch_bounds__(kThreadsI, 1)
       }
     }
   }
+  if (prof && lane == 0) {
+    const long long tot = clock64() - t_start;
+    for (int i = 0; i < 4; ++i) atomicAdd(prof + warp * 5 + i, (unsigned long long)wt[i]);
+    atomicAdd(prof + warp * 5 + 4, (unsigned long long)tot);
+  }
+#undef DFNO_W
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -491,8 +505,22 @@ int yzt_inv_tc2(const dfno_geom& g, const void* in, double scale, void* out, cud
       cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int grid = sm_count_i() < slabs ? sm_count_i() : slabs;
-  k_yzt_inv_tc2<<<grid, kThreadsI, L.total + 1024, st>>>(g, (const float2*)in, mo, (float)scale);
+  static unsigned long long* prof = nullptr;
+  static const bool want_prof = getenv("DFNO_WAIT_PROFILE") && getenv("DFNO_WAIT_PROFILE")[0] == '1';
+  if (want_prof && !prof) cudaMalloc(&prof, kWarpsI * 5 * sizeof(unsigned long long));
+  if (prof) cudaMemsetAsync(prof, 0, kWarpsI * 5 * sizeof(unsigned long long), st);
+  k_yzt_inv_tc2<<<grid, kThreadsI, L.total + 1024, st>>>(g, (const float2*)in, mo, (float)scale, prof);
   DFNO_CUDA_CHECK_LAUNCH();
+  if (prof) {  // debug: per-warp wait cycles averaged over CTAs
+    unsigned long long h[kWarpsI * 5];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "yzt_inv_tc2: per-CTA avg cycles  [w0 w1 w2 w3 | total]\n");
+    for (int w = 0; w < kWarpsI; ++w)
+      fprintf(stderr, "  warp %2d: %9.0f %9.0f %9.0f %9.0f | %9.0f\n", w, h[w * 5] / (double)grid,
+              h[w * 5 + 1] / (double)grid, h[w * 5 + 2] / (double)grid, h[w * 5 + 3] / (double)grid,
+              h[w * 5 + 4] / (double)grid);
+  }
   return DFNO_OK;
 }
 

@@ -226,6 +226,15 @@ __device__ __forceinline__ void tma_load_4d(void* sdst, const void* tmap, int c0
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16),
+// completion counted on `bar` (tx bytes).
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // 2-D TMA tile load global -> shared, completion counted on `bar` (tx bytes).
 __device__ __forceinline__ void tma_load_2d(void* sdst, const void* tmap, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -293,7 +302,11 @@ __device__ __forceinline__ void split_hl(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
-// ---- cp.async (LDGSTS): 16-byte and 4-byte copies with zero fill ---------
+// ---- cp.async (LDGSTS): 16-, 8- and 4-byte copies with zero fill ---------
+__device__ __forceinline__ void cp8(void* sdst, const void* gsrc, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(valid ? 8 : 0)
+               : "memory");
+}
 __device__ __forceinline__ void cp16(void* sdst, const void* gsrc, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc),
                "r"(valid ? 16 : 0)
