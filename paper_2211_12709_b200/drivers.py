@@ -17,6 +17,12 @@ finite-difference gradient check (criterion 3) run unchanged on B200:
                         along random parameter directions (d/bench.py:229-280)
   drive_comm_volume     measured repartition traffic == predicted_block_volume
                         (d/bench.py:314-356), integer-exact
+  make_dataset          the synthetic spectral-propagator problem
+                        (d/bench.py:403-430): same PCG64 draws, transforms
+                        and mixing in float64 on the device
+  drive_train           a full training run on it (d/bench.py:433-508):
+                        train_step epochs, globally reduced test MSE / MAE /
+                        R^2 per epoch, optional checkpoint
 """
 
 from __future__ import annotations
@@ -42,7 +48,8 @@ from .fno import (
     slice_local,
 )
 from .partition import Partition
-from .spectral import ModeSpec
+from .spectral import ModeSpec, retained_indices
+from .training import AdamState, global_output_count, train_step
 from .tensor import DATA_LABELS, DenseTensor, DimLabel, DType
 
 
@@ -235,4 +242,93 @@ def drive_comm_volume(comm: Communicator, opts: dict) -> Optional[dict]:
             "bytes_per_element": p.bytes_per_element}
 
 
-__all__ = ["config_from_opts", "drive_parity_forward", "drive_adjoint", "drive_gradient", "drive_comm_volume"]
+def make_dataset(config: FnoConfig, samples: int, seed: int, device=None) -> tuple:
+    """(inputs, targets) of the synthetic problem (reference d/bench.py:403-430):
+    white-noise inputs pushed through a fixed random truncated-spectral
+    propagator.  The random draws are the reference's (numpy PCG64, same
+    order and shapes); the transforms and the per-mode channel mixing run in
+    float64 on ``device``; both tensors are returned there in the config's
+    real dtype, shaped (samples, c, Nx, Ny, Nz, Nt)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    rng = np.random.default_rng(seed)
+    keep = [torch.from_numpy(retained_indices(n, m)).to(dev) for n, m in zip(config.grid, config.mode_counts)]
+    r_shape = tuple(len(k) for k in keep)
+    cin, cout = config.in_channels, config.out_channels
+    scale = 1.0 / np.sqrt(2.0 * cin)
+    prop = scale * (rng.standard_normal((cout, cin) + r_shape) + 1j * rng.standard_normal((cout, cin) + r_shape))
+    inputs = torch.from_numpy(rng.standard_normal((samples, cin) + config.grid)).to(dev)
+    spec = torch.fft.fftn(inputs, dim=(2, 3, 4, 5))
+    for d, k in enumerate(keep):
+        spec = spec.index_select(2 + d, k)
+    mixed = torch.einsum("bixyzt,oixyzt->boxyzt", spec, torch.from_numpy(prop).to(dev))
+    padded = torch.zeros((samples, cout) + config.grid, dtype=torch.complex128, device=dev)
+    kx, ky, kz, kt = keep
+    padded[:, :, kx[:, None, None, None], ky[None, :, None, None], kz[None, None, :, None], kt[None, None, None, :]] = mixed
+    targets = torch.fft.ifftn(padded, dim=(2, 3, 4, 5)).real
+    real = torch.float32 if config.dtype == DType.REAL32 else torch.float64
+    return inputs.to(real).contiguous(), targets.to(real).contiguous()
+
+
+def drive_train(comm: Communicator, opts: dict) -> Optional[dict]:
+    """Training run on the synthetic problem (reference d/bench.py:433-508).
+    Every rank regenerates the dataset from the seed and keeps its x slab on
+    the device; the per-epoch rows are globally reduced, so they do not
+    depend on the rank count."""
+    config = config_from_opts(opts)
+    seed = opts["seed"]
+    n_train, n_test = opts.get("train_samples", 200), opts.get("test_samples", 50)
+    batch, lr, epochs = opts.get("batch", 10), opts.get("lr", 2e-3), opts.get("epochs", 50)
+    stop_r2 = opts.get("early_stop_r2")
+    dev = _device(comm)
+    inputs, targets = make_dataset(config, n_train + n_test, seed + 9000, device=dev)
+    my_x = config.x_partition().range_of(comm.rank).as_slice()
+    inputs, targets = inputs[:, :, my_x].contiguous(), targets[:, :, my_x].contiguous()
+
+    def local_pair(lo: int, hi: int) -> tuple:
+        return DenseTensor(DATA_LABELS, inputs[lo:hi]), DenseTensor(DATA_LABELS, targets[lo:hi])
+
+    params = shard_params(init_params(config, seed, device=dev), config, comm.rank)
+    state = AdamState()
+    test_t = targets[n_train:].double()
+    test_count = global_output_count(config, n_test)
+    test_mean = comm.allreduce_sum_scalar(float(test_t.sum()), label="tr.mean") / test_count
+    sst_local = float(((test_t - test_mean) ** 2).sum())
+
+    def evaluate() -> tuple:
+        sse = sae = 0.0
+        for lo in range(n_train, n_train + n_test, batch):
+            x_local, t_local = local_pair(lo, min(lo + batch, n_train + n_test))
+            resid = (fno_forward(comm, x_local, params, config).data - t_local.data).double()
+            sse += float((resid * resid).sum())
+            sae += float(resid.abs().sum())
+        sse = comm.allreduce_sum_scalar(sse, label="ev.sse")
+        sae = comm.allreduce_sum_scalar(sae, label="ev.sae")
+        sst = comm.allreduce_sum_scalar(sst_local, label="ev.sst")
+        return sse / test_count, sae / test_count, 1.0 - sse / sst
+
+    mse0, mae0, r20 = evaluate()
+    metrics = [{"epoch": 0, "train_mse_median": None, "test_mse": mse0, "test_mae": mae0, "test_r2": r20}]
+    for epoch in range(1, epochs + 1):
+        losses = []
+        for lo in range(0, n_train, batch):
+            x_local, t_local = local_pair(lo, min(lo + batch, n_train))
+            params, loss = train_step(comm, x_local, t_local, params, state, lr, config)
+            losses.append(loss)
+        mse, mae, r2 = evaluate()
+        metrics.append({"epoch": epoch, "train_mse_median": float(np.median(losses)), "test_mse": mse,
+                        "test_mae": mae, "test_r2": r2})
+        if stop_r2 is not None and r2 > stop_r2:
+            break
+    if opts.get("checkpoint"):
+        from .dtns import gather_params, save_checkpoint
+
+        full = gather_params(comm, params, config)
+        if comm.rank == 0:
+            save_checkpoint(opts["checkpoint"], full, config, seed)
+    if comm.rank != 0:
+        return None
+    return {"metrics": metrics, "epochs_run": metrics[-1]["epoch"]}
+
+
+__all__ = ["config_from_opts", "drive_parity_forward", "drive_adjoint", "drive_gradient", "drive_comm_volume",
+           "make_dataset", "drive_train"]

@@ -216,6 +216,30 @@ def training_case():
     print("training", list(out))
 
 
+TRAIN_OPTS = {"grid": [8, 8, 8, 4], "modes": [2, 2, 2, 2], "channels": 3, "in_channels": 1, "out_channels": 1,
+              "blocks": 2, "dtype": "real32", "seed": 13, "train_samples": 6, "test_samples": 3, "batch": 2,
+              "lr": 3e-2, "epochs": 4}
+
+
+def train_case():
+    """The reference's synthetic dataset (d/bench.py:403-430) and a short
+    drive_train run (d/bench.py:433-508) at P = 1 and P = 2."""
+    from distfno.bench import make_dataset
+
+    cfg = cfg_of((8, 8, 8, 4), (2, 2, 2, 2), 3, 2, "real32", 1, cin=1, cout=2)
+    x, y = make_dataset(cfg, 3, 77)
+    out = {"ds_x": x, "ds_y": y}
+    meta = {"dataset": {"grid": [8, 8, 8, 4], "modes": [2, 2, 2, 2], "channels": 3, "in_channels": 1,
+                        "out_channels": 2, "blocks": 2, "dtype": "real32", "workers": 1, "samples": 3, "seed": 77},
+            "opts": TRAIN_OPTS}
+    for P in (1, 2):
+        res = run_distributed("train", dict(TRAIN_OPTS, workers=P), P, "inproc")
+        meta[f"train_p{P}"] = res
+    np.savez_compressed(OUT / "train_ref.npz", **out)
+    (OUT / "train_ref.json").write_text(json.dumps(meta, indent=1))
+    print("train", meta["train_p1"]["metrics"][-1], meta["train_p2"]["metrics"][-1])
+
+
 def dtns_case():
     """The reference's DTNS bytes (d/tensor.py:258-320) for four dtypes and
     a reference checkpoint directory (d/training.py:176-208)."""
@@ -248,10 +272,14 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dtns":
         dtns_case()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "train":
+        train_case()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "training":
         training_case()
         sys.exit(0)
     training_case()
+    train_case()
     dtns_case()
     partitions()
     init_digests()

@@ -45,3 +45,39 @@ def test_finite_difference_gradient():
     res = run(D.drive_gradient, {"grid": [8, 8, 8, 4], "modes": [2, 2, 2, 2], "channels": 2, "blocks": 2,
                                  "dtype": "real64", "seed": 11, "directions": 5, "workers": 2})
     assert res["max_rel_err"] < 1e-5, res["errors"]
+
+
+@pytest.fixture(scope="module")
+def train_ref(golden_dir):
+    import numpy as np
+
+    return json.loads((golden_dir / "train_ref.json").read_text()), np.load(golden_dir / "train_ref.npz")
+
+
+def test_make_dataset_matches_reference(train_ref):
+    meta, arrays = train_ref
+    d = meta["dataset"]
+    x, y = D.make_dataset(D.config_from_opts(d), d["samples"], d["seed"])
+    assert x.is_cuda and x.dtype == y.dtype
+    assert (x.cpu().numpy() == arrays["ds_x"]).all()  # same PCG64 draws, cast once
+    err = abs(y.cpu().numpy() - arrays["ds_y"]).max() / abs(arrays["ds_y"]).max()
+    assert err < 1e-6  # float64 transforms on the device vs numpy, then one float32 rounding
+
+
+@pytest.mark.parametrize("workers", [1, 2])
+def test_drive_train_matches_reference(train_ref, workers, tmp_path):
+    meta, _ = train_ref
+    opts = dict(meta["opts"], workers=workers, checkpoint=str(tmp_path / "ckpt"))
+    got = run(D.drive_train, opts)
+    want = meta[f"train_p{workers}"]
+    assert got["epochs_run"] == want["epochs_run"] == len(want["metrics"]) - 1
+    for g, w in zip(got["metrics"], want["metrics"]):
+        assert g["epoch"] == w["epoch"]
+        for k in ("test_mse", "test_mae", "test_r2", "train_mse_median"):
+            if w[k] is None:
+                assert g[k] is None
+            else:  # float32 training, 4 epochs of Adam: agreement to ~1e-6 relative
+                assert abs(g[k] - w[k]) <= 1e-4 * max(abs(w[k]), 1e-2), (k, g[k], w[k])
+    assert got["metrics"][-1]["test_mse"] < 0.7 * got["metrics"][0]["test_mse"]  # it learns
+    params, cfg, seed = P.load_checkpoint(str(tmp_path / "ckpt"))
+    assert seed == opts["seed"] and cfg.num_ranks == workers
