@@ -20,6 +20,8 @@
 // streams the weights with full occupancy and no block-wide phases; the
 // extra traffic is the 2 x b c r_x (ky) r_z r_t spectrum round trip
 // (21 MB at C2 against 210 MB of weights).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace dfno {
@@ -202,6 +204,108 @@ __global__ void __launch_bounds__(kXT) k_xmix_bwd(const dfno_geom g, const float
   }
 }
 
+// Two (kx, m) columns per thread (16-byte loads and stores): the contractions
+// are weight-stream bound and latency-limited at the occupancy their register
+// blocking allows, so doubling the bytes per request doubles the bytes in
+// flight.  Requires an even column count (r_x * modes).
+__device__ __forceinline__ void cmac2(float4& acc, const float4& a, const float4& b) {
+  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(a.y, b.x, acc.y);
+  acc.z = fmaf(a.z, b.z, acc.z); acc.z = fmaf(-a.w, b.w, acc.z);
+  acc.w = fmaf(a.z, b.w, acc.w); acc.w = fmaf(a.w, b.z, acc.w);
+}
+__device__ __forceinline__ void cmac2_conj_a(float4& acc, const float4& a, const float4& b) {  // conj(a) b
+  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y); acc.y = fmaf(-a.y, b.x, acc.y);
+  acc.z = fmaf(a.z, b.z, acc.z); acc.z = fmaf(a.w, b.w, acc.z);
+  acc.w = fmaf(a.z, b.w, acc.w); acc.w = fmaf(-a.w, b.z, acc.w);
+}
+__device__ __forceinline__ void cmac2_conj_b(float4& acc, const float4& a, const float4& b) {  // a conj(b)
+  acc.x = fmaf(a.x, b.x, acc.x); acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.y, b.x, acc.y); acc.y = fmaf(-a.x, b.y, acc.y);
+  acc.z = fmaf(a.z, b.z, acc.z); acc.z = fmaf(a.w, b.w, acc.z);
+  acc.w = fmaf(a.w, b.z, acc.w); acc.w = fmaf(-a.z, b.w, acc.w);
+}
+
+__global__ void __launch_bounds__(kXT, 3) k_xmix2(const dfno_geom g, const float4* __restrict__ X,
+                                               const float4* __restrict__ W, float4* __restrict__ Y) {
+  const long long mloc = mloc_of(g);
+  const int C = g.c, nog = (C + kOG - 1) / kOG;
+  const long long cols = (long long)g.rx * mloc / 2;  // column pairs
+  const long long n = (long long)nog * cols;
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long col = e % cols;
+    const int o0 = (int)(e / cols) * kOG;
+    for (int bb = 0; bb < g.batch; ++bb) {
+      float4 acc[kOG];
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4* xp = X + ((long long)bb * C) * cols + col;
+#pragma unroll 2
+      for (int i = 0; i < C; ++i) {
+        const float4 xv = xp[(long long)i * cols];
+        const float4* wr = W + ((long long)i * C + o0) * cols + col;
+#pragma unroll
+        for (int j = 0; j < kOG; ++j) {
+          const float4 wv = (o0 + j < C) ? __ldcs(wr + j * cols) : make_float4(0.f, 0.f, 0.f, 0.f);
+          cmac2(acc[j], xv, wv);
+        }
+      }
+      float4* yp = Y + ((long long)bb * C + o0) * cols + col;
+#pragma unroll
+      for (int j = 0; j < kOG; ++j)
+        if (o0 + j < C) yp[j * cols] = acc[j];
+    }
+  }
+}
+
+template <int BM>
+__global__ void __launch_bounds__(kXT, 3) k_xmix_bwd2(const dfno_geom g, const float4* __restrict__ S,
+                                                   const float4* __restrict__ D, const float4* __restrict__ W,
+                                                   float4* __restrict__ gW, float4* __restrict__ dX) {
+  const long long mloc = mloc_of(g);
+  const int C = g.c, nig = (C + kOG - 1) / kOG, B = g.batch;
+  const long long cols = (long long)g.rx * mloc / 2;
+  const long long n = (long long)nig * cols;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
+    const long long col = e % cols;
+    const int i0 = (int)(e / cols) * kOG;
+    float4 sv[BM][kOG], dx[BM][kOG];
+#pragma unroll
+    for (int bb = 0; bb < BM; ++bb)
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) {
+        sv[bb][j] = (bb < B && i0 + j < C) ? S[((long long)bb * C + i0 + j) * cols + col] : z4;
+        dx[bb][j] = z4;
+      }
+#pragma unroll 2
+    for (int o = 0; o < C; ++o) {
+      float4 dv[BM];
+#pragma unroll
+      for (int bb = 0; bb < BM; ++bb) dv[bb] = (bb < B) ? D[((long long)bb * C + o) * cols + col] : z4;
+#pragma unroll
+      for (int j = 0; j < kOG; ++j) {
+        if (i0 + j >= C) continue;
+        const long long wi = ((long long)(i0 + j) * C + o) * cols + col;
+        const float4 wv = __ldcs(W + wi);
+        float4 gacc = z4;
+#pragma unroll
+        for (int bb = 0; bb < BM; ++bb) {
+          cmac2_conj_a(gacc, sv[bb][j], dv[bb]);  // conj(S) D
+          cmac2_conj_b(dx[bb][j], dv[bb], wv);    // D conj(W)
+        }
+        __stcs(gW + wi, gacc);
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < BM; ++bb)
+#pragma unroll
+      for (int j = 0; j < kOG; ++j)
+        if (bb < B && i0 + j < C) dX[((long long)bb * C + i0 + j) * cols + col] = dx[bb][j];
+  }
+}
+
 int xdft_tc(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st);
 int xidft_tc(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st);
 
@@ -217,6 +321,149 @@ int sms_x() {
   return n;
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked x-DFTs (SIMT, N_x <= 128, r_x <= 16).  Both are small
+// complex GEMMs (16 x N_x by N_x x modes) that the FFMA issue rate bounds, so
+// each thread owns two modes (m, m + 32: coalesced across the warp) and eight
+// kx (forward) or all sixteen kx (inverse): every twiddle read from shared
+// memory (broadcast float4 = 2 twiddles) feeds 8 complex MACs, every data
+// load 8 or 16.  A block covers 256 modes of one (b, c).  Twiddles are fp32
+// sincospif (<= 1 ulp) with the exact integer phase reduction.
+constexpr int kXM = 256;
+constexpr int kXB = 256;  // threads per block
+
+__device__ __forceinline__ void fill_tw16(float2* tw, long long* rows, const dfno_geom& g, int bb, int c) {
+  for (int e = threadIdx.x; e < g.nx * 16; e += blockDim.x) {
+    const int x = e >> 4, k = e & 15;
+    float sn = 0.f, cs = 0.f;
+    if (k < g.rx) {
+      const long long f = mode_freq(k, g.nx, g.mx);
+      const long long idx = ((f % g.nx + g.nx) % g.nx) * x % g.nx;
+      sincospif(2.0f * (float)idx / (float)g.nx, &sn, &cs);
+    }
+    tw[e] = make_float2(cs, -sn);  // e^{-2 pi i f x / Nx}
+  }
+  for (int x = threadIdx.x; x < g.nx; x += blockDim.x) rows[x] = kx_row(g, bb, c, x);
+}
+
+__global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2* __restrict__ kx_in, float s1,
+                                                float2* __restrict__ X) {
+  extern __shared__ __align__(16) unsigned char xs_raw[];
+  const int Nx = g.nx;
+  float2* tw = reinterpret_cast<float2*>(xs_raw);  // [Nx][16]
+  long long* rows = reinterpret_cast<long long*>(tw + Nx * 16);
+  const long long mloc = mloc_of(g);
+  const long long mtiles = (mloc + kXM - 1) / kXM;
+  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kXM;
+  const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
+  fill_tw16(tw, rows, g, bb, c);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, kh = w & 1;
+  const long long ma = m0 + (w >> 1) * 64 + lane, mb = ma + 32;
+  const bool oka = ma < mloc, okb = mb < mloc;
+  float2 acc[2][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[0][j] = acc[1][j] = make_float2(0.f, 0.f);
+  const float4* t4 = reinterpret_cast<const float4*>(tw) + 4 * kh;
+  // loads run four x ahead of the MACs (register double buffer)
+  constexpr int kPf = 4;
+  float2 za[kPf], zb[kPf];
+  auto fetch = [&](int x0) {
+#pragma unroll
+    for (int u = 0; u < kPf; ++u) {
+      const int x = x0 + u;
+      const float2* src = kx_in + rows[x < Nx ? x : 0];
+      za[u] = (oka && x < Nx) ? __ldcs(src + ma) : make_float2(0.f, 0.f);
+      zb[u] = (okb && x < Nx) ? __ldcs(src + mb) : make_float2(0.f, 0.f);
+    }
+  };
+  fetch(0);
+#pragma unroll 1
+  for (int x0 = 0; x0 < Nx; x0 += kPf) {
+    float2 ca[kPf], cb[kPf];
+#pragma unroll
+    for (int u = 0; u < kPf; ++u) {
+      ca[u] = za[u];
+      cb[u] = zb[u];
+    }
+    fetch(x0 + kPf);
+#pragma unroll
+    for (int u = 0; u < kPf; ++u) {
+      const int x = min(x0 + u, Nx - 1);  // x >= Nx carries zero data
+#pragma unroll
+      for (int j2 = 0; j2 < 4; ++j2) {
+        const float4 t = t4[x * 8 + j2];
+        const float2 t0 = make_float2(t.x, t.y), t1 = make_float2(t.z, t.w);
+        cmac<float>(acc[0][2 * j2], ca[u], t0);
+        cmac<float>(acc[0][2 * j2 + 1], ca[u], t1);
+        cmac<float>(acc[1][2 * j2], cb[u], t0);
+        cmac<float>(acc[1][2 * j2 + 1], cb[u], t1);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int kx = 8 * kh + j;
+    if (kx < g.rx) {
+      float2* dst = X + (bc * g.rx + kx) * mloc;
+      if (oka) dst[ma] = make_float2(s1 * acc[0][j].x, s1 * acc[0][j].y);
+      if (okb) dst[mb] = make_float2(s1 * acc[1][j].x, s1 * acc[1][j].y);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kXB) k_xidft_s(const dfno_geom g, const float2* __restrict__ Y, float s2,
+                                                 float2* __restrict__ kx_out) {
+  extern __shared__ __align__(16) unsigned char xs_raw[];
+  const int Nx = g.nx;
+  float2* tw = reinterpret_cast<float2*>(xs_raw);  // [Nx][16]
+  long long* rows = reinterpret_cast<long long*>(tw + Nx * 16);
+  const long long mloc = mloc_of(g);
+  const long long mtiles = (mloc + kXM - 1) / kXM;
+  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kXM;
+  const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xh = w & 1;
+  const long long ma = m0 + (w >> 1) * 64 + lane, mb = ma + 32;
+  const bool oka = ma < mloc, okb = mb < mloc;
+  float2 ya[16], yb[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const float2* src = Y + (bc * g.rx + k) * mloc;
+    ya[k] = (oka && k < g.rx) ? __ldg(src + ma) : make_float2(0.f, 0.f);
+    yb[k] = (okb && k < g.rx) ? __ldg(src + mb) : make_float2(0.f, 0.f);
+  }
+  fill_tw16(tw, rows, g, bb, c);
+  __syncthreads();
+  const float4* t4 = reinterpret_cast<const float4*>(tw);
+  const int xa = xh ? (Nx + 1) / 2 : 0, xb = xh ? Nx : (Nx + 1) / 2;
+#pragma unroll 2
+  for (int x = xa; x < xb; ++x) {
+    float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      const float4 t = t4[x * 8 + k2];
+      const float2 t0 = make_float2(t.x, t.y), t1 = make_float2(t.z, t.w);
+      cmac_conj_b<float>(a, ya[2 * k2], t0);  // e^{+i} = conj(e^{-i})
+      cmac_conj_b<float>(a, ya[2 * k2 + 1], t1);
+      cmac_conj_b<float>(b, yb[2 * k2], t0);
+      cmac_conj_b<float>(b, yb[2 * k2 + 1], t1);
+    }
+    float2* dst = kx_out + rows[x];
+    if (oka) __stcs(dst + ma, make_float2(s2 * a.x, s2 * a.y));
+    if (okb) __stcs(dst + mb, make_float2(s2 * b.x, s2 * b.y));
+  }
+}
+
+int xdft_mode() {  // 0: tiled SIMT (default), 1: tcgen05, for A/B measurements (DFNO_XDFT=tc)
+  static const int v = [] {
+    const char* e = getenv("DFNO_XDFT");
+    return (e && e[0] == 't') ? 1 : 0;
+  }();
+  return v;
+}
+
+bool tiled_ok(const dfno_geom& g) { return g.dtype == DFNO_F32 && g.rx <= 16 && g.nx <= 128; }
+
 unsigned grid_for(long long n, int per_sm = 8) {
   long long b = (n + kXT - 1) / kXT;
   const long long cap = (long long)sms_x() * per_sm;
@@ -224,6 +471,14 @@ unsigned grid_for(long long n, int per_sm = 8) {
 }
 
 int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
+  if (tiled_ok(g) && xdft_mode() == 0) {
+    const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
+    const long long blocks = (long long)g.batch * g.c * ((mloc + kXM - 1) / kXM);
+    const size_t smem = (size_t)g.nx * 16 * sizeof(float2) + (size_t)g.nx * sizeof(long long);
+    k_xdft_s<<<(unsigned)blocks, kXB, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);
+    DFNO_CUDA_CHECK_LAUNCH();
+    return DFNO_OK;
+  }
   const int rc = xdft_tc(g, kx_in, s1, X, st);  // tcgen05 path (N_x <= 128, r_x <= 16)
   if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
@@ -237,6 +492,14 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
 }
 
 int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
+  if (tiled_ok(g) && xdft_mode() == 0) {
+    const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
+    const long long blocks = (long long)g.batch * g.c * ((mloc + kXM - 1) / kXM);
+    const size_t smem = (size_t)g.nx * 16 * sizeof(float2) + (size_t)g.nx * sizeof(long long);
+    k_xidft_s<<<(unsigned)blocks, kXB, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);
+    DFNO_CUDA_CHECK_LAUNCH();
+    return DFNO_OK;
+  }
   const int rc = xidft_tc(g, Y, s2, kx_out, st);
   if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
@@ -268,8 +531,12 @@ int xspec_fwd_stream(const dfno_geom& g, const void* kx_in, const void* w, void*
   int rc = launch_dft(g, kx_in, 1.f, X, st);  // fft_x unnormalised (d/spectral.py:36)
   if (rc) return rc;
   const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
-  k_xmix<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(g, (const float2*)X,
-                                                                              (const float2*)w, (float2*)Y);
+  if (cols % 2 == 0)
+    k_xmix2<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(g, (const float4*)X,
+                                                                                    (const float4*)w, (float4*)Y);
+  else
+    k_xmix<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(g, (const float2*)X,
+                                                                                (const float2*)w, (float2*)Y);
   DFNO_CUDA_CHECK_LAUNCH();
   return launch_idft(g, Y, (float)(1.0 / g.nx), kx_out, st);  // ifft_x carries 1/Nx (d/spectral.py:49)
 }
@@ -283,9 +550,14 @@ int xspec_bwd_stream(const dfno_geom& g, const void* kx_in, const void* spec, co
   int rc = launch_dft(g, kx_in, (float)(1.0 / g.nx), D, st);  // fft_x / Nx (d/fno.py:450-452)
   if (rc) return rc;
   const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
-  auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
-  kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(
-      g, (const float2*)spec, (const float2*)D, (const float2*)w, (float2*)gw, (float2*)dX);
+  if (cols % 2 == 0 && g.batch == 1) {
+    k_xmix_bwd2<1><<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(
+        g, (const float4*)spec, (const float4*)D, (const float4*)w, (float4*)gw, (float4*)dX);
+  } else {
+    auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
+    kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(
+        g, (const float2*)spec, (const float2*)D, (const float2*)w, (float2*)gw, (float2*)dX);
+  }
   DFNO_CUDA_CHECK_LAUNCH();
   return launch_idft(g, dX, 1.f, kx_out, st);  // ifft_x * Nx = unnormalised inverse (d/fno.py:455-457)
 }
