@@ -123,27 +123,49 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.monotonic(), line))
 
     def start(self):
+        """Start nvidia-smi (20 ms period) and return once it is producing
+        samples, so the timed region that follows is covered."""
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        threading.Thread(target=self._reader, daemon=True).start()
+        deadline = time.monotonic() + 10.0
+        while not self.lines and time.monotonic() < deadline:
+            time.sleep(0.01)
+
+    def mark(self):
+        """Call right before the timed region starts."""
+        self.t0 = time.monotonic()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.t1 = time.monotonic()
+        time.sleep(0.05)  # the sample in flight at the end of the region
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-            out, _ = self.proc.communicate()
+        t0 = self.t0 if self.t0 is not None else 0.0
+        window = [ln for t, ln in self.lines if t0 - 0.025 <= t <= self.t1 + 0.025]
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in window:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -156,7 +178,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "period_ms": 20}
 
 
 class KernelTimer:
@@ -258,6 +280,7 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
+    clocks.mark()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()

@@ -427,10 +427,10 @@ __global__ void __launch_bounds__(kMbThreads, 4) k_mix_fwd_tc(long long npts, in
 constexpr int kMfMaxStages = 8;
 
 template <int CM, bool EXACT, int ACT>
-__global__ void __launch_bounds__(kMbThreads + 32, 3)
+__global__ void __launch_bounds__(kMbThreads + 32, 4)
     k_mix_fwd_tma(long long npts, int nb, int cin_rt, int cout_rt, const __grid_constant__ CUtensorMap tm_src,
                   const __grid_constant__ CUtensorMap tm_pre, const __grid_constant__ CUtensorMap tm_post, int src_act,
-                  const float* __restrict__ w, int has_post, int nstages) {
+                  const float* __restrict__ w, int has_post, int nstages, int nbuf) {
   const int cin = EXACT ? CM : cin_rt, cout = EXACT ? CM : cout_rt;
   // dynamic: ring[nstages][cin][128] | pre staging[2][cout][128] | post staging[2][cout][128]
   extern __shared__ __align__(1024) unsigned char dyn[];
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kMbThreads + 32, 3)
   const int stage_bytes = cin * kMbThreads * 4, out_bytes = cout * kMbThreads * 4;
   unsigned char* ring = dyn;
   float* stage_pre = reinterpret_cast<float*>(dyn + nstages * stage_bytes);
-  float* stage_post = reinterpret_cast<float*>(dyn + nstages * stage_bytes + 2 * out_bytes);
+  float* stage_post = reinterpret_cast<float*>(dyn + nstages * stage_bytes + nbuf * out_bytes);
 
   if (warp == 4) {
     // ---- TMA producer
@@ -495,8 +495,8 @@ __global__ void __launch_bounds__(kMbThreads + 32, 3)
       uint32_t r[32];
       tc::tmem_ld32_nowait(dcol(k) + lane_off, r);
       tc::tmem_ld_wait();
-      float* sp = stage_pre + (k & 1) * (out_bytes / 4) + tid;
-      float* sq = stage_post + (k & 1) * (out_bytes / 4) + tid;
+      float* sp = stage_pre + (k & (nbuf - 1)) * (out_bytes / 4) + tid;
+      float* sq = stage_post + (k & (nbuf - 1)) * (out_bytes / 4) + tid;
 #pragma unroll
       for (int o = 0; o < CM; ++o) {
         if (EXACT || o < cout) {
@@ -512,8 +512,8 @@ __global__ void __launch_bounds__(kMbThreads + 32, 3)
       const long long tile = blockIdx.x + (long long)k * gridDim.x;
       const long long bb = tile / tiles_per_b;
       const int p0 = (int)((tile - bb * tiles_per_b) * kMbThreads), r0 = (int)(bb * cout);
-      tc::tma_store_2d(&tm_pre, stage_pre + (k & 1) * (out_bytes / 4), p0, r0);
-      if (has_post) tc::tma_store_2d(&tm_post, stage_post + (k & 1) * (out_bytes / 4), p0, r0);
+      tc::tma_store_2d(&tm_pre, stage_pre + (k & (nbuf - 1)) * (out_bytes / 4), p0, r0);
+      if (has_post) tc::tma_store_2d(&tm_post, stage_post + (k & (nbuf - 1)) * (out_bytes / 4), p0, r0);
       tc::bulk_commit();
     };
     int it = 0;
@@ -555,16 +555,22 @@ __global__ void __launch_bounds__(kMbThreads + 32, 3)
           tc::mma_tf32_ts(d, ah + 8 * k, bl, id, 1u);
         }
         tc::commit(&bar);
-        if (it >= 2) store(it - 2);  // staged by every worker before the barrier above
+        if (nbuf == 2 && it >= 2) store(it - 2);  // staged by every worker before the barrier above
       }
-      if (it > 0) drain(it - 1);
+      if (it > 0) {
+        drain(it - 1);
+        if (nbuf == 1) {  // single staging buffer: store it now; the next drain waits for its read
+          tc::named_sync(1, kMbThreads);
+          if (tid == 0) store(it - 1);
+        }
+      }
     }
     if (it > 0) {
       tc::mbar_wait(&bar, (it - 1) & 1);
       tc::fence_after();
       if (tid == 0) tc::bulk_wait_read0();
       tc::named_sync(1, kMbThreads);
-      if (tid == 0 && it >= 2) store(it - 2);
+      if (tid == 0 && nbuf == 2 && it >= 2) store(it - 2);
       drain(it - 1);
       tc::named_sync(1, kMbThreads);
       if (tid == 0) {
@@ -599,23 +605,31 @@ static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const v
       (!post || make_rows_map(&tm_post, post, npts, (long long)nb * cout, cout))) {
     if (!post) tm_post = tm_pre;
     // per-CTA dynamic shared memory: ring + double-buffered output staging;
-    // 3 CTAs per SM when a ring of >= 2 stages fits, else 2
-    const int stage_bytes = cin * kMbThreads * 4, out_bytes = cout * kMbThreads * 4 * 2 * (post ? 2 : 1);
+    // up to 4 CTAs per SM (the TMEM limit at 128 columns each) while a ring
+    // of >= 2 stages fits
+    const int stage_bytes = cin * kMbThreads * 4, out_one = cout * kMbThreads * 4 * (post ? 2 : 1);
     const int static_bytes = 2 * 4096 + 256;
-    int per_sm = 3, stages = 0;
-    for (; per_sm >= 1; --per_sm) {
-      const int avail = (227 * 1024) / per_sm - 1024 - static_bytes - out_bytes;
-      stages = avail / stage_bytes;
+    static const int max_per_sm = [] {
+      const char* e = getenv("DFNO_MF_CTAS");
+      const int v = e ? atoi(e) : 4;
+      return v < 1 ? 1 : (v > 4 ? 4 : v);
+    }();
+    int per_sm = max_per_sm, stages = 0, nbuf = 2;
+    for (; per_sm >= 1; --per_sm) {  // double-buffered staging first, then single
+      for (nbuf = 2; nbuf >= 1; --nbuf) {
+        stages = ((227 * 1024) / per_sm - 1024 - static_bytes - nbuf * out_one) / stage_bytes;
+        if (stages >= 2) break;
+      }
       if (stages >= 2) break;
     }
     if (stages > 4) stages = 4;
     if (per_sm >= 1 && stages >= 2) {
-      const int smem = stages * stage_bytes + out_bytes;
+      const int smem = stages * stage_bytes + nbuf * out_one;
       auto kt = k_mix_fwd_tma<CM, EXACT, ACT>;
       if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
         const long long grid = tiles < (long long)per_sm * sms ? tiles : (long long)per_sm * sms;
         kt<<<(unsigned)grid, kMbThreads + 32, smem, st>>>(npts, nb, cin, cout, tm_src, tm_pre, tm_post, src_act,
-                                                          (const float*)w, post ? 1 : 0, stages);
+                                                          (const float*)w, post ? 1 : 0, stages, nbuf);
         DFNO_CUDA_CHECK_LAUNCH();
         return DFNO_OK;
       }
