@@ -184,6 +184,31 @@ def test_mix_forward_backward(dtype, cin, cout):
         assert O.rel_err(gw.cpu().numpy(), np.einsum("bip,bop->io", xs, gp)) < t * 10
 
 
+@pytest.mark.parametrize("cin,cout", [(20, 20), (1, 20), (20, 3)])
+@pytest.mark.parametrize("with_post", [True, False])
+def test_mix_forward_tma_paths(cin, cout, with_post):
+    """npts % 4 == 0 selects the TMA-fed mix kernel (TMA loads, double-buffered
+    TMEM accumulators, TMA stores; single-buffered staging when the output
+    activation is also written); odd tails exercise the clipped last tile."""
+    b, npts = 2, 4100
+    g = geom((8, 8, 8, 4), (2, 2, 2, 2), c=20, batch=b, dtype=_lib.F32, cin=cin, cout=cout)
+    rng = np.random.default_rng(5)
+    x = torch.tensor(rng.standard_normal((b, cin, npts)), dtype=torch.float32, device="cuda")
+    w = torch.tensor(rng.standard_normal((cin, cout)), dtype=torch.float32, device="cuda")
+    pre = torch.full((b, cout, npts), float("nan"), device="cuda")
+    post = torch.full_like(pre, float("nan")) if with_post else None
+    for src_act in (0, 1):
+        call("dfno_mix_fwd", ctypes.byref(g), npts, cin, cout, _lib.ptr(x), src_act, _lib.ptr(w), _lib.ptr(pre),
+             _lib.ptr(post) if with_post else None, None)
+        xs = x.double().cpu().numpy()
+        if src_act:
+            xs = O.act("gelu", xs)
+        want = np.einsum("bip,io->bop", xs, w.double().cpu().numpy())
+        assert O.rel_err(pre.cpu().numpy(), want) < 1e-5
+        if with_post:
+            assert O.rel_err(post.cpu().numpy(), O.act("gelu", want)) < 1e-5
+
+
 def test_full_size_round_trip_and_linearity():
     """C2 geometry (64^3 x 32, c = 20): size-independent properties.
     (1) band-limited round trip: yzt_inv(yzt_fwd(u)) == u for u made of
