@@ -103,3 +103,20 @@ def test_non_finite_loss_raises_before_update():
     with pytest.raises(P.NonFiniteLossError):
         T.train_step(comm, x, P.DenseTensor(P.DATA_LABELS, y), params, st, 1e-3, cfg)
     assert st.step == 0 and not st.m
+
+
+def test_adam_vectorized_path_bit_identical_to_scalar_path():
+    """n % 4 == 0 takes the 16-byte kernel; an n % 4 != 0 tensor with the same
+    leading elements takes the golden-pinned scalar kernel: identical bits."""
+    rng = np.random.default_rng(7)
+    p0 = rng.standard_normal(4097).astype(np.float32)
+    st4, st1 = T.AdamState(), T.AdamState()
+    p4 = P.DenseTensor(("x",), torch.from_numpy(p0[:4096].copy()).cuda())
+    p1 = P.DenseTensor(("x",), torch.from_numpy(p0.copy()).cuda())
+    for k in range(3):
+        g = (rng.standard_normal(4097) * 10.0 ** (-k)).astype(np.float32)
+        st4.step += 1
+        st1.step += 1
+        p4 = T.adam_update(st4, "w", p4, P.DenseTensor(("x",), torch.from_numpy(g[:4096].copy()).cuda()), 1e-3)
+        p1 = T.adam_update(st1, "w", p1, P.DenseTensor(("x",), torch.from_numpy(g.copy()).cuda()), 1e-3)
+        assert torch.equal(p4.data.view(torch.int32), p1.data[:4096].view(torch.int32)), f"step {k + 1}"

@@ -59,7 +59,7 @@ def main(tag):
         tot = sum(sum(v) for v in d.values())
         with open(P / f"{tag}_launches.txt", "w") as fh:
             fh.write("ncu --metrics gpu__time_duration.sum --clock-control none -c 400  python bench.py --steps 2 "
-                     "--warmup 1 --no-cpu-baseline --no-e2e  (all launches of 3 steps; cold, serialised)\n")
+                     "--warmup 1 --no-cpu-baseline --no-e2e  (every launch of the command: 3 fwd+bwd steps plus the train-step measurement; cold, serialised)\n")
             fh.write(f"{'n':>4} {'avg_us':>9} {'total_ms':>9} {'share':>6} kernel\n")
             for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
                 fh.write(f"{len(v):4d} {sum(v) / len(v) / 1e3:9.1f} {sum(v) / 1e6:9.3f} {sum(v) / tot:6.3f} {k}\n")
