@@ -12,7 +12,7 @@
 // accumulators in registers.  The weight gradient is a (cin x cout) reduction
 // over all points: per-CTA register-tiled 4x4 partial sums, reduced across
 // point groups with warp shuffles + shared memory, written as one partial per
-// CTA and summed in fixed order by k_reduce_partials (deterministic).
+// CTA and summed in a fixed order by k_reduce_partials8 (deterministic).
 #include "common.cuh"
 
 namespace dfno {
@@ -272,13 +272,24 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
   }
 }
 
+// Fixed-shape tree over the partials (deterministic, independent of
+// scheduling): 32 consecutive elements per warp (coalesced), eight warps take
+// every eighth partial, then the eight group sums are added pairwise.
 template <typename R>
-__global__ void k_reduce_partials(int nparts, long long n, const R* __restrict__ partials, R* __restrict__ out) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    R s = (R)0;
-    for (int k = 0; k < nparts; ++k) s += partials[(long long)k * n + e];
-    out[e] = s;
+__global__ void __launch_bounds__(256) k_reduce_partials8(int nparts, long long n, const R* __restrict__ partials,
+                                                          R* __restrict__ out) {
+  __shared__ R grp_sum[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const long long e = (long long)blockIdx.x * 32 + lane;
+  R s = (R)0;
+  if (e < n)
+    for (int k = grp; k < nparts; k += 8) s += partials[(long long)k * n + e];
+  grp_sum[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && e < n) {
+    const R a = (grp_sum[0][lane] + grp_sum[1][lane]) + (grp_sum[2][lane] + grp_sum[3][lane]);
+    const R b = (grp_sum[4][lane] + grp_sum[5][lane]) + (grp_sum[6][lane] + grp_sum[7][lane]);
+    out[e] = a + b;
   }
 }
 
@@ -491,11 +502,11 @@ extern "C" int dfno_reduce_partials(const dfno_geom* g, int num_partials, int64_
                                     void* stream) {
   if (!g || !partials || !out) return DFNO_ERR_NULL;
   cudaStream_t st = (cudaStream_t)stream;
-  const int blocks = (int)((n + 255) / 256);
+  const int blocks = (int)((n + 31) / 32);
   if (g->dtype == DFNO_F32)
-    k_reduce_partials<float><<<blocks, 256, 0, st>>>(num_partials, n, (const float*)partials, (float*)out);
+    k_reduce_partials8<float><<<blocks, 256, 0, st>>>(num_partials, n, (const float*)partials, (float*)out);
   else if (g->dtype == DFNO_F64)
-    k_reduce_partials<double><<<blocks, 256, 0, st>>>(num_partials, n, (const double*)partials, (double*)out);
+    k_reduce_partials8<double><<<blocks, 256, 0, st>>>(num_partials, n, (const double*)partials, (double*)out);
   else
     return DFNO_ERR_DTYPE;
   DFNO_CUDA_CHECK_LAUNCH();

@@ -16,7 +16,7 @@
 //        points yields all four hi/lo cross products; D2 accumulates over
 //        every tile of the CTA in TMEM and the three significant quadrants
 //        are summed once at the end into this CTA's partial (reduced in fixed
-//        order by k_reduce_partials: deterministic, d/training.py:77-82).
+//        order by k_reduce_partials8: deterministic, d/training.py:77-82).
 //        Rows 64..127 of the A2 operand alias B2 (their D2 rows are never
 //        read).
 //
