@@ -13,8 +13,8 @@
 // Per slab (b, c, x):
 //   loader  warp 20: V (16 contiguous (kz, kt) blocks per slab) -> shared, bulk
 //           copies one slab ahead
-//   front   warps 0-3: V -> A_Y (TMEM), rows (kz, kt) [2 tiles], K = (ky re | ky im)
-//   MMA Y'  D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (TS, N=32,
+//   front   warps 0-3: V -> A_Y (shared), rows (kz, kt) [2 tiles], K = (ky re | ky im)
+//   MMA Y'  D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (SS, N=32,
 //           16 y per pass)
 //   front   D_Y -> stash1 -> A_T[(y 8, kz)][(kt re | kt im)] (TMEM) per 8-y chunk
 //   MMA T'  D_T[(y,kz)][t re 32 | t im 32] = A_T . [[C,-S];[S,C]]_t  (TS, N=64)
