@@ -102,6 +102,7 @@ def alg_bytes(cfg, xl, kyl, nranks):
         "mix_fwd.dec": A + 2 * Aout,
         "yzt_fwd.fwd": A + T_xk,
         "yzt_fwd.bwd": 2 * A + T_xk,
+        "yzt_fwd.bwd_raw": A + T_xk,  # last block: act' fused into the decoder's mix_bwd
         "xspec_fwd": T_kx + W + S + T_kx,
         "xspec_bwd": T_kx + S + W + W + T_kx,
         "yzt_inv.fwd": T_xk + A,

@@ -118,6 +118,10 @@ int dfno_mix_fwd(const dfno_geom* g, int64_t npts, int cin, int cout,
  *   gp = gout * act'(pre)
  *   gin[b][i][p] = sum_o gp[b][o][p] * w[i][o]            (gin may be NULL)
  *   partials[k][i][o] = CTA k's share of sum_{b,p} f(src[b][i][p]) gp[b][o][p]
+ * src_act: 0 f = id, 1 f = act, 2 f = act and gin is returned multiplied by
+ * act'(src) -- the gradient w.r.t. src itself, i.e. the decoder backward
+ * fused with the last block's activation derivative (fp32 tcgen05 path only;
+ * DFNO_ERR_UNSUPPORTED elsewhere, and the caller then uses 1).
  * dfno_mix_bwd_partials() gives the partial-buffer element count;
  * dfno_reduce_partials() then sums the partials in a fixed order
  * (deterministic, bit-identical replicas: d/training.py:77-82).

@@ -483,7 +483,13 @@ extern "C" int dfno_mix_bwd(const dfno_geom* g, int64_t npts, int cin, int cout,
                             const void* src, int src_act, const void* w, void* gin, void* partials, void* stream) {
   if (!g || !gout || !pre || !src || !w || !partials) return DFNO_ERR_NULL;
   if (npts < 1 || cin < 1 || cout < 1) return DFNO_ERR_DIMENSION;
+  if (src_act < 0 || src_act > 2) return DFNO_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
+  if (src_act == 2) {  // fused act'(src) on the input gradient: tcgen05 path only
+    if (g->dtype != DFNO_F32 || !mix_tc_enabled() || !gin) return DFNO_ERR_UNSUPPORTED;
+    return mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
+                      mix_bwd_blocks(npts, g->batch), st);
+  }
   if (g->dtype == DFNO_F32) {
     if (mix_tc_enabled()) {
       const int rc = mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,

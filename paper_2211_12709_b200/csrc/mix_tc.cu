@@ -92,6 +92,14 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   int it = 0;
   long long prev_out = -1;  // gin element offset of the previous tile's point (or -1)
 
+  // src_act == 2: the input gradient leaves already multiplied by act'(src)
+  // (the decoder's input is the last block's pre-activation, so the next
+  // backward DFT needs no act' of its own); dprev holds act'(src) of the tile
+  // being drained
+  const bool gin_dact = src_act == 2;
+  float dprev[CM], dcur[CM];
+#pragma unroll
+  for (int i = 0; i < CM; ++i) dprev[i] = dcur[i] = 1.f;
   auto drain_gin = [&]() {
     uint32_t r[32];
     tc::tmem_ld32_nowait(d1 + lane_off, r);
@@ -99,7 +107,10 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     if (prev_out >= 0) {
 #pragma unroll
       for (int i = 0; i < CM; ++i)
-        if (EXACT || i < cin) __stcs(gin + prev_out + (long long)i * npts, __uint_as_float(r[i]));
+        if (EXACT || i < cin) {
+          const float v = __uint_as_float(r[i]);
+          __stcs(gin + prev_out + (long long)i * npts, gin_dact ? v * dprev[i] : v);
+        }
     }
   };
 
@@ -136,7 +147,13 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     // gp = g * act'(pre) ; a = act(src) or src  (zero for padding / invalid points)
 #pragma unroll
     for (int o = 0; o < CM; ++o) gp[o] = gv[o] * act_deriv<float>(ACT, pv[o]);
-    if (src_act) {
+    if (gin_dact) {
+#pragma unroll
+      for (int i = 0; i < CM; ++i) {
+        a[i] = act_apply<float>(ACT, sv[i]);
+        dcur[i] = act_deriv<float>(ACT, sv[i]);
+      }
+    } else if (src_act) {
 #pragma unroll
       for (int i = 0; i < CM; ++i) a[i] = act_apply<float>(ACT, sv[i]);
     } else {
@@ -150,6 +167,8 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       tc::fence_after();
       if (want_gin) drain_gin();
     }
+#pragma unroll
+    for (int i = 0; i < CM; ++i) dprev[i] = dcur[i];
     {
       // gp split once (round-to-nearest hi, exact remainder lo; the tensor
       // core's truncation of lo costs <= 2^-21 relative) and shared by the

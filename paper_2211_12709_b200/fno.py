@@ -400,15 +400,31 @@ class _Plan:
             self.gp, self.npts, cin, cout, _lib.ptr(src), int(src_act), _lib.ptr(w), _lib.ptr(pre), _lib.ptr(post),
             _lib.stream_handle()), "dfno_mix_fwd"))
 
-    def mix_bwd(self, cin, cout, gout, pre, src, src_act, w, gin, tag="mix_bwd") -> torch.Tensor:
+    def mix_bwd(self, cin, cout, gout, pre, src, src_act, w, gin, tag="mix_bwd", fuse_src_dact=False):
+        """Mixer backward; with ``fuse_src_dact`` (src_act must be true) the
+        library is first asked for gin * act'(src) in the same pass (status
+        DFNO_ERR_UNSUPPORTED outside the tcgen05 envelope).  Returns (gw, fused)."""
         buf, nparts = self.partial_buf(cin, cout)
-        _launch(f"mix_bwd.{tag}", lambda: _lib.check(self.lib.dfno_mix_bwd(
-            self.gp, self.npts, cin, cout, _lib.ptr(gout), _lib.ptr(pre), _lib.ptr(src), int(src_act), _lib.ptr(w),
-            _lib.ptr(gin), _lib.ptr(buf), _lib.stream_handle()), "dfno_mix_bwd"))
+        fused = [False]
+
+        def run():
+            args = (self.gp, self.npts, cin, cout, _lib.ptr(gout), _lib.ptr(pre), _lib.ptr(src))
+            tail = (_lib.ptr(w), _lib.ptr(gin), _lib.ptr(buf), _lib.stream_handle())
+            if fuse_src_dact:
+                rc = self.lib.dfno_mix_bwd(*args, 2, *tail)
+                if rc == _DFNO_ERR_UNSUPPORTED:
+                    rc = self.lib.dfno_mix_bwd(*args, 1, *tail)
+                else:
+                    fused[0] = rc == 0
+            else:
+                rc = self.lib.dfno_mix_bwd(*args, int(src_act), *tail)
+            _lib.check(rc, "dfno_mix_bwd")
+
+        _launch(f"mix_bwd.{tag}", run)
         gw = torch.empty((cin, cout), dtype=self.real, device=self.device)
         _launch(f"reduce.{tag}", lambda: _lib.check(self.lib.dfno_reduce_partials(
             self.gp, nparts, cin * cout, _lib.ptr(buf), _lib.ptr(gw), _lib.stream_handle()), "dfno_reduce_partials"))
-        return gw
+        return (gw, fused[0]) if fuse_src_dact else gw
 
     def yzt_fwd(self, src, pre, mode, scale, out, tag="yzt_fwd"):
         _launch(tag, lambda: _lib.check(self.lib.dfno_dft_yzt_fwd(
@@ -455,6 +471,9 @@ def set_kernel_timer(timer) -> None:
     bench.py to time kernels with CUDA events); None removes it."""
     global _TIMER
     _TIMER = timer
+
+
+_DFNO_ERR_UNSUPPORTED = -7  # include/dfno.h
 
 
 def _launch(name: str, fn) -> None:
@@ -641,7 +660,8 @@ def _block_backward(comm, plan: _Plan, g: torch.Tensor, pre: Optional[torch.Tens
     """Adjoint chain (reference fno.py:445-464): fft_yzt/N_yzt -> truncate ->
     R(x->ky) -> fft_x/Nx -> truncate -> gW, dX -> pad -> ifft_x*Nx -> R(ky->x)
     -> pad -> ifft_yzt*N_yzt -> real."""
-    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a, tag="yzt_fwd.bwd")
+    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a,
+                 tag="yzt_fwd.bwd" if mode == _lib.SRC_GRAD else "yzt_fwd.bwd_raw")
     kx_in = plan.x_to_ky(comm, f"{label}.bwd.x->ky")
     gw = torch.empty(plan.w_shape, dtype=plan.cplx, device=plan.device)
     plan.xspec_bwd(kx_in, spec, w, gw, plan.buf_c)
@@ -679,14 +699,19 @@ def fno_backward(comm: Communicator, g_local: DenseTensor, params: FnoParams, co
     dec_w = _on_device(cache.dec_w, plan, plan.real, "decoder weight")
     last_pre = cache.blocks[-1].pre_activation.data
     g_a = plan.empty_act(c)
-    gwd_local = plan.mix_bwd(c, config.out_channels, g, cache.dec_pre.data, last_pre, True, dec_w, g_a, tag="dec")
+    # the decoder's input is act(last block output): when the library fuses
+    # act'(last_pre) into the decoder's input gradient, the last block's
+    # backward DFT reads one stream (RAW) instead of g and pre (GRAD)
+    gwd_local, fused = plan.mix_bwd(c, config.out_channels, g, cache.dec_pre.data, last_pre, True, dec_w, g_a,
+                                    tag="dec", fuse_src_dact=True)
 
     block_grads = [None] * L
     for i in reversed(range(L)):
         bc = cache.blocks[i]
         w = _check_weight(params.blocks[i], plan, f"block{i} weight")
-        g_a, gw = _block_backward(comm, plan, g_a, bc.pre_activation.data, _lib.SRC_GRAD, w, bc.spec_in.data,
-                                  f"block{i}")
+        raw = fused and i == L - 1
+        g_a, gw = _block_backward(comm, plan, g_a, None if raw else bc.pre_activation.data,
+                                  _lib.SRC_RAW if raw else _lib.SRC_GRAD, w, bc.spec_in.data, f"block{i}")
         block_grads[i] = DenseTensor(params.blocks[i].labels, gw)
 
     enc_w = _on_device(cache.enc_w, plan, plan.real, "encoder weight")
