@@ -209,6 +209,36 @@ def test_mix_forward_tma_paths(cin, cout, with_post):
             assert O.rel_err(post.cpu().numpy(), O.act("gelu", want)) < 1e-5
 
 
+def test_mix_backward_fused_src_activation_derivative():
+    """src_act = 2: gin comes back multiplied by act'(src) (the decoder backward
+    fused with the last block's activation derivative); same weight gradient
+    as src_act = 1."""
+    b, npts, cin, cout = 2, 4100, 20, 20
+    g = geom((8, 8, 8, 4), (2, 2, 2, 2), c=20, batch=b, dtype=_lib.F32, cin=cin, cout=cout)
+    rng = np.random.default_rng(6)
+    src = torch.tensor(rng.standard_normal((b, cin, npts)), dtype=torch.float32, device="cuda")
+    pre = torch.tensor(rng.standard_normal((b, cout, npts)), dtype=torch.float32, device="cuda")
+    gout = torch.tensor(rng.standard_normal((b, cout, npts)), dtype=torch.float32, device="cuda")
+    w = torch.tensor(rng.standard_normal((cin, cout)), dtype=torch.float32, device="cuda")
+    n, k = ctypes.c_int64(), ctypes.c_int()
+    call("dfno_mix_bwd_partials", ctypes.byref(g), npts, cin, cout, ctypes.byref(n), ctypes.byref(k))
+    out = {}
+    for sa in (1, 2):
+        parts = torch.empty(n.value, device="cuda")
+        gin = torch.empty_like(src)
+        call("dfno_mix_bwd", ctypes.byref(g), npts, cin, cout, _lib.ptr(gout), _lib.ptr(pre), _lib.ptr(src), sa,
+             _lib.ptr(w), _lib.ptr(gin), _lib.ptr(parts), None)
+        gw = torch.empty((cin, cout), device="cuda")
+        call("dfno_reduce_partials", ctypes.byref(g), k.value, cin * cout, _lib.ptr(parts), _lib.ptr(gw), None)
+        out[sa] = (gin.double().cpu().numpy(), gw.cpu().numpy())
+    s64 = src.double().cpu().numpy()
+    gp = gout.double().cpu().numpy() * O.act_grad("gelu", pre.double().cpu().numpy())
+    gin_a = np.einsum("bop,io->bip", gp, w.double().cpu().numpy())
+    assert O.rel_err(out[1][0], gin_a) < 1e-5
+    assert O.rel_err(out[2][0], gin_a * O.act_grad("gelu", s64)) < 1e-5
+    assert np.array_equal(out[1][1], out[2][1])
+
+
 def test_full_size_round_trip_and_linearity():
     """C2 geometry (64^3 x 32, c = 20): size-independent properties.
     (1) band-limited round trip: yzt_inv(yzt_fwd(u)) == u for u made of
