@@ -54,6 +54,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-train", action="store_true")
     p.add_argument("--sample-ranks", type=int, default=16, help="CPU sample: 1/R of the job per process")
+    p.add_argument("--config", choices=["auto", "C3", "C4rank"], default="auto",
+                   help="auto: C2 at N = 1, C5 weak scaling under torchrun; C3: 128^3x32 on one GPU; C4rank: the "
+                        "CO2 grid 262x118x64x86 as 8 thread-ranks on one GPU (every launch has a P = 8 rank's "
+                        "geometry)")
     return p.parse_args()
 
 
@@ -186,12 +190,15 @@ class KernelTimer:
     """CUDA-event pairs around every libdfno launch (current stream)."""
 
     def __init__(self):
+        import threading
+
         import torch
 
         self.torch = torch
         self.events = {}
         self.launches = 0
         self.enabled = True
+        self.lock = threading.Lock()  # thread-ranks share the stream: keep each event pair tight
 
     def __call__(self, name, fn):
         if not self.enabled:
@@ -199,11 +206,12 @@ class KernelTimer:
             return
         t = self.torch.cuda
         s, e = t.Event(enable_timing=True), t.Event(enable_timing=True)
-        s.record()
-        fn()
-        e.record()
-        self.events.setdefault(name, []).append((s, e))
-        self.launches += 1
+        with self.lock:
+            s.record()
+            fn()
+            e.record()
+            self.events.setdefault(name, []).append((s, e))
+            self.launches += 1
 
     def summary(self):
         out = {}
@@ -442,6 +450,114 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+SINGLE_GPU_CONFIGS = {
+    # name: (grid, thread-ranks, workload)
+    "C3": ((128, 128, 128, 32), 1, "C3 3-D Navier-Stokes FNO 128x128x128x32, width 20, 4 blocks, modes 8, batch 1, "
+                                   "fwd+bwd, one B200"),
+    "C4rank": ((262, 118, 64, 86), 8, "C4 CO2 FNO 262x118x64x86 (1.98 M cells x 86 steps), width 20, 4 blocks, "
+                                      "modes 8, batch 1, fwd+bwd, as 8 thread-ranks on one B200 (x slabs 33x6 + "
+                                      "32x2, ky pencils of 2)"),
+}
+
+
+def run_single_gpu_config(args):
+    """C3 / C4rank: the north-star grids on one GPU.  C4rank runs the P = 8
+    decomposition as thread-ranks sharing the GPU (ThreadWorld), so every
+    kernel launch has exactly one P = 8 rank's geometry; ``value`` is samples/s
+    of the whole C4 problem on one GPU and each kernel's roofline is per launch."""
+    import threading
+
+    import torch
+
+    import paper_2211_12709_b200 as P
+    from paper_2211_12709_b200 import fno as F
+
+    grid, ranks, wname = SINGLE_GPU_CONFIGS[args.config]
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    cfg = P.FnoConfig(*grid, CHANNELS, CHANNELS, CHANNELS, P.ModeSpec.of_xyzt(*MODES), BLOCKS, "gelu", "real32",
+                      ranks)
+    full = P.init_params(cfg, SEED, device=dev)
+    torch.manual_seed(SEED)
+    xpart = cfg.x_partition()
+    timer = KernelTimer()
+    clocks = ClockSampler(0)
+    times = {}
+    lock = threading.Lock()
+
+    def body(comm):
+        r = comm.rank
+        params = P.shard_params(full, cfg, r)
+        x = P.DenseTensor(P.DATA_LABELS, torch.randn((1, CHANNELS, xpart.extent_of(r)) + grid[1:], device=dev))
+
+        def step():
+            cache = P.ForwardCache()
+            y = P.fno_forward(comm, x, params, cfg, cache)
+            P.fno_backward(comm, y, params, cfg, cache)
+
+        for _ in range(args.warmup):
+            step()
+        comm.barrier()
+        if r == 0:
+            torch.cuda.synchronize()
+            F.set_kernel_timer(timer)
+            clocks.start()
+            clocks.mark()
+            times["t0"] = torch.cuda.Event(enable_timing=True)
+            times["t0"].record()
+        comm.barrier()
+        for _ in range(args.steps):
+            step()
+        comm.barrier()
+        if r == 0:
+            times["t1"] = torch.cuda.Event(enable_timing=True)
+            times["t1"].record()
+            torch.cuda.synchronize()
+            F.set_kernel_timer(None)
+        comm.barrier()
+        with lock:
+            times.setdefault("xl", {})[r] = (xpart.extent_of(r), cfg.ky_partition().extent_of(r))
+
+    P.run_ranks(ranks, body)
+    clock_info = clocks.stop()
+    ms = times["t0"].elapsed_time(times["t1"]) / args.steps
+    ksum = timer.summary()
+    hbm, hbm_kind = peaks()
+    # per-launch algorithmic bytes: launches alternate over ranks; use the
+    # busiest rank's geometry (x_r = 33 / ky_r = 2 at C4, every rank at C3)
+    xl = max(v[0] for v in times["xl"].values())
+    kyl = max(v[1] for v in times["xl"].values())
+    ab = alg_bytes(cfg, xl, kyl, ranks)
+    # mean per-launch bytes over ranks (uneven x slabs)
+    ab_mean = {k: sum(alg_bytes(cfg, v[0], v[1], ranks)[k] for v in times["xl"].values()) / ranks for k in ab}
+    kernels = {k: {"launches_per_step": n / args.steps, "avg_ms": round(t / n, 5),
+                   "share": round(t / sum(v[1] for v in ksum.values()), 4),
+                   "alg_GBps": round(ab_mean[k] / (t / n * 1e-3) / 1e9, 1) if ab_mean[k] else None,
+                   "roofline_frac": round(ab_mean[k] / (t / n * 1e-3) / 1e9 / hbm, 4) if ab_mean[k] else None}
+               for k, (n, t) in sorted(ksum.items(), key=lambda kv: -kv[1][1])}
+    dname, (dn, dms) = max(ksum.items(), key=lambda kv: kv[1][1])
+    achieved = ab_mean[dname] / (dms / dn * 1e-3) / 1e9
+    step_bytes = sum(ab_mean[k] * n / args.steps for k, (n, _) in ksum.items())
+    result = {
+        "metric": f"FNO fwd+bwd samples/s ({args.config} problem, whole job on one GPU)",
+        "value": round(1e3 / ms, 4), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic: x ~ N(0,1), weights = reference init_params(seed 42), g = y",
+        "config": {"workload": wname, "grid": list(grid), "channels": CHANNELS, "modes": list(MODES),
+                   "blocks": BLOCKS, "batch": 1, "thread_ranks": ranks,
+                   "l2": "activations larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1), "peak": hbm,
+                     "peak_kind": hbm_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "alg_bytes_per_launch": int(ab_mean[dname]), "avg_launch_ms": round(dms / dn, 5),
+                     "traffic": None},
+        "step_roofline": {"alg_bytes_per_step": int(step_bytes),
+                          "achieved_GBps": round(step_bytes / (ms * 1e-3) / 1e9, 1),
+                          "frac": round(step_bytes / (ms * 1e-3) / 1e9 / hbm, 4)},
+        "kernels": kernels, "gpu_launches": int(timer.launches), "clocks": clock_info,
+    }
+    print(json.dumps(result), flush=True)
+
+
 def cpu_baseline(grid, ranks, steps):
     from oracle import cpu_baseline as cb
 
@@ -489,5 +605,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config != "auto":
+        run_single_gpu_config(a)
     else:
         run_ours(a)

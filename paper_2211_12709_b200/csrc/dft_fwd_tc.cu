@@ -61,7 +61,7 @@ constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
 constexpr int kAYPlane = 16 * 512;                  // 128 rows x K 16, SBO 512 (one hi or lo plane of one tile)
 constexpr int kAYBytes = 4 * kAYPlane;              // 2 tiles x (hi, lo)
 
-// TMEM column map (512): A_T 2x64 | D1 2x32 | A_Z 2x64 | D2 2x64 (hi.hi+lo.hi | hi.lo) | D3 2 tiles x 32
+// TMEM column map (512): A_T 2x64 | D1 2x32 | A_Z 2x64 | D2 2x64 (hi.hi | hi.lo+lo.hi) | D3 2 tiles x 32
 constexpr uint32_t cAT = 0, cD1 = 128, cAZ = 192, cD2 = 320, cD3 = 448;
 
 struct Lay {
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::fence_before();
       tc::mbar_arrive(&d2_empty[cb]);
       {
-        const int yl = 2 * q + yy, kt = lo16;  // D2 row (y_l, kt): (hi.hi + lo.hi) + hi.lo
+        const int yl = 2 * q + yy, kt = lo16;  // D2 row (y_l, kt): hi.hi + (hi.lo + lo.hi)
 #pragma unroll
         for (int kz = 0; kz < 16; ++kz) {
           stash[((0 * 16 + kz) * 16 + kt) * 9 + yl] = __uint_as_float(u0[kz]);
@@ -431,14 +431,19 @@ __global__ void __launch_bounds__(kThreads2, 1)
           DFNO_W(1, tc::mbar_wait(&at_full[ab], (i >> 1) & 1));
           tc::fence_after();
           const uint32_t a = tmem + cAT + 64 * ab, d = tmem + cD1 + 32 * b;
+          // lo products first, hi.hi last: the accumulator's adds are not
+          // round-to-nearest, so only the hi.hi sums should meet a
+          // full-magnitude accumulator
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const uint32_t kb = (uint32_t)(tb * 4 + s) * 256;
             const uint64_t bh = tc::desc(sbt + kb, 128, L.sbo_t), bl = tc::desc(sbt + plt + kb, 128, L.sbo_t);
-            tc::mma_tf32_ts(d, a + 8 * s, bh, id, (tb | s) ? 1u : 0u);
-            tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
+            tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, (tb | s) ? 1u : 0u);
             tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
           }
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbt + (uint32_t)(tb * 4 + s) * 256, 128, L.sbo_t), id, 1u);
           tc::commit(&at_empty[ab]);
         }
         tc::commit(&d1_full[b]);
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int s = 0; s < 4; ++s) {
           const uint64_t bb = tc::desc(sbz + (uint32_t)(gi.zb * 4 + s) * 256, 128, L.sbo_z);
           tc::mma_tf32_ts(d, a + 8 * s, bb, id64, (gi.zb | s) ? 1u : 0u);  // hi.[hi | lo]
-          tc::mma_tf32_ts(d, a + 32 + 8 * s, bb, id32, 1u);               // lo.hi
+          tc::mma_tf32_ts(d + 32, a + 32 + 8 * s, bb, id32, 1u);          // lo.hi, with hi.lo
         }
         tc::commit(&az_empty[b]);
         if (gi.zb == L.nzb - 1) {

@@ -367,15 +367,23 @@ __global__ void __launch_bounds__(kThreads3, 1)
           for (int hh = 0; hh < 2; ++hh) {
             const uint32_t d = tmem + jDY + 32 * hh;
             const uint32_t ah0 = say + (2 * hh) * kAYPlane3, al0 = ah0 + kAYPlane3;
+            // the small lo products first, the hi.hi products last: the
+            // accumulator's non-round-to-nearest adds then bias only the
+            // last four sums at full magnitude
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
               const uint32_t kb = (uint32_t)s * 256;
               const uint64_t ah = tc::desc(ah0 + kb, 128, 1024), al = tc::desc(al0 + kb, 128, 1024);
               const uint64_t bh = tc::desc(sby + (uint32_t)p * 4096 + kb, 128, 1024);
               const uint64_t bl = tc::desc(sby + L.by_plane + (uint32_t)p * 4096 + kb, 128, 1024);
-              tc::mma_tf32(d, ah, bh, id, s ? 1u : 0u);
-              tc::mma_tf32(d, al, bh, id, 1u);
+              tc::mma_tf32(d, al, bh, id, s ? 1u : 0u);
               tc::mma_tf32(d, ah, bl, id, 1u);
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const uint32_t kb = (uint32_t)s * 256;
+              tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + (uint32_t)p * 4096 + kb, 128, 1024), id,
+                           1u);
             }
           }
           tc::commit(&dy_full);
@@ -395,13 +403,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::fence_after();
         const uint32_t a = tmem + jAT, d = tmem + jDT + 64 * b;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
+        for (int s = 0; s < 4; ++s) {  // lo products first, hi.hi last (see the Y' issuer)
           const uint32_t kb = (uint32_t)s * 256;
           const uint64_t bh = tc::desc(sbt + kb, 128, 1024), bl = tc::desc(sbt + 8 * 1024 + kb, 128, 1024);
-          tc::mma_tf32_ts(d, a + 8 * s, bh, id, s ? 1u : 0u);
-          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
+          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, s ? 1u : 0u);
           tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
         }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbt + (uint32_t)s * 256, 128, 1024), id, 1u);
         tc::commit(&dt_full[b]);
         tc::commit(&at_empty);
       }
@@ -432,13 +441,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::fence_after();
         const uint32_t a = tmem + jAZ + 64 * k, d = tmem + jDZ + 64 * k;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
+        for (int s = 0; s < 4; ++s) {  // lo products first, hi.hi last (see the Y' issuer)
           const uint32_t kb = (uint32_t)s * 256;
           const uint64_t bh = tc::desc(sbz + kb, 128, 1024), bl = tc::desc(sbz + 8 * 1024 + kb, 128, 1024);
-          tc::mma_tf32_ts(d, a + 8 * s, bh, id, s ? 1u : 0u);
-          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, 1u);
+          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, s ? 1u : 0u);
           tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
         }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbz + (uint32_t)s * 256, 128, 1024), id, 1u);
         tc::commit(&dz_full[k]);
         tc::commit(&az_empty[k]);
       }

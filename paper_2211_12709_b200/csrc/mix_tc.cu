@@ -13,12 +13,17 @@
 //   GEMM2 (weight grad)  D2[r][c] += sum_p A2[r][p] B2[c][p]
 //        rows r: a_hi(i) at r = i, a_lo(i) at r = 32 + i; columns c: gp_hi(o)
 //        at c = o, gp_lo(o) at c = 32 + o, so ONE M=128 N=64 K=8 MMA per 8
-//        points yields all four hi/lo cross products; D2 accumulates over
-//        every tile of the CTA in TMEM and the three significant quadrants
-//        are summed once at the end into this CTA's partial (reduced in fixed
-//        order by k_reduce_partials8: deterministic, d/training.py:77-82).
-//        Rows 64..127 of the A2 operand alias B2 (their D2 rows are never
-//        read).
+//        points yields all four hi/lo cross products.  D2 accumulates kMbFlush
+//        tiles in TMEM, then warps 0-1 fold its quadrants into a per-CTA
+//        accumulator (TMEM columns 192..223, round-to-nearest fp32 adds in
+//        registers) and the next tile restarts D2: the
+//        tensor core's fp32 accumulation is not round-to-nearest, and left to
+//        run over a whole CTA's share of points (~3.5k MMAs at C2) its bias
+//        cost 7.5e-5 relative on the weight gradient against a random upstream
+//        gradient (tools/precision_probe.py).  The folded sums become this CTA's
+//        partial (reduced in fixed order by k_reduce_partials8: deterministic,
+//        d/training.py:77-82).  Rows 64..127 of the A2 operand alias B2 (their
+//        D2 rows are never read).
 //
 // Shared-memory operands are SWIZZLE_NONE K-major with a padded LBO of 144 B
 // so the one-point-per-thread scalar stores are bank-conflict free.  The MMAs
@@ -34,7 +39,8 @@ constexpr int kMbThreads = 128;             // one thread per point of a 128-poi
 constexpr int kMbLbo = 144;                 // bytes between K-adjacent core matrices
 constexpr int kMbSbo = 32 * kMbLbo;         // bytes between 8-row groups (K = 128 points)
 constexpr int kMbOpBytes = 8 * kMbSbo;      // 64 rows x 128 points
-constexpr uint32_t kMbTmemCols = 256;       // D1 0..31 | A1 hi 32..63 | A1 lo 64..95 | D2 128..191
+constexpr uint32_t kMbTmemCols = 256;       // D1 0..31 | A1 hi 32..63 | A1 lo 64..95 | D2 128..191 | ACC 192..223
+constexpr int kMbFlush = 16;                // tiles (2048 points) accumulated in D2 before the fold into ACC
 
 __device__ __forceinline__ int mb_off(int r, int k) {
   return (r >> 3) * kMbSbo + (k >> 2) * kMbLbo + (r & 7) * 16 + (k & 3) * 4;
@@ -84,7 +90,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
-  const uint32_t d1 = tmem, a1h = tmem + 32, a1l = tmem + 64, d2 = tmem + 128;
+  const uint32_t d1 = tmem, a1h = tmem + 32, a1l = tmem + 64, d2 = tmem + 128, dacc = tmem + 192;
   const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
 
   const long long tiles_per_b = (npts + kMbThreads - 1) / kMbThreads;
@@ -112,6 +118,30 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
           __stcs(gin + prev_out + (long long)i * npts, gin_dact ? v * dprev[i] : v);
         }
     }
+  };
+
+  // fold D2 (rows 0..63: a_hi(i), a_lo(i); columns gp_hi(o) | gp_lo(o)) into
+  // ACC[row][o] (TMEM); warps 0-1, row = thread
+  bool acc_live = false;
+  auto fold_d2 = [&]() {
+    if (warp < 2) {
+      uint32_t r0[32], r1[32];
+      float v[32];
+      tc::tmem_ld32_nowait(d2 + lane_off, r0);
+      tc::tmem_ld32_nowait(d2 + lane_off + 32, r1);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r0[c]) + __uint_as_float(r1[c]);
+      if (acc_live) {
+        tc::tmem_ld32_nowait(dacc + lane_off, r0);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] += __uint_as_float(r0[c]);
+      }
+      tc::tmem_st32(dacc + lane_off, v);
+      tc::tmem_st_wait();
+    }
+    acc_live = true;
   };
 
   // register double buffer: tile i + 1 is loaded while tile i is converted
@@ -166,6 +196,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       tc::mbar_wait(&bar2, (it - 1) & 1);
       tc::fence_after();
       if (want_gin) drain_gin();
+      if ((it - 1) % kMbFlush == kMbFlush - 1) fold_d2();  // D2 restarts at tile it
     }
 #pragma unroll
     for (int i = 0; i < CM; ++i) dprev[i] = dcur[i];
@@ -208,13 +239,13 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       tc::fence_after();
       const uint32_t id1 = tc::idesc_tf32(128, NPi);
       const uint32_t sb1 = tc::smem_u32(b1);
-      for (int s = 0; s < KPo / 8; ++s) {
+      for (int s = 0; s < KPo / 8; ++s) {  // lo products first, hi.hi last
         const uint64_t bh = tc::desc(sb1 + s * 256, 128, sbo_b1);
         const uint64_t bl = tc::desc(sb1 + b1_plane + s * 256, 128, sbo_b1);
-        tc::mma_tf32_ts(d1, a1h + 8 * s, bh, id1, s > 0 ? 1u : 0u);
-        tc::mma_tf32_ts(d1, a1l + 8 * s, bh, id1, 1u);
+        tc::mma_tf32_ts(d1, a1l + 8 * s, bh, id1, s > 0 ? 1u : 0u);
         tc::mma_tf32_ts(d1, a1h + 8 * s, bl, id1, 1u);
       }
+      for (int s = 0; s < KPo / 8; ++s) tc::mma_tf32_ts(d1, a1h + 8 * s, tc::desc(sb1 + s * 256, 128, sbo_b1), id1, 1u);
       tc::commit(&bar);
     }
     if (tid == 32) {  // second issuing warp: the weight-gradient GEMM overlaps GEMM1's issue
@@ -224,7 +255,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
 #pragma unroll 4
       for (int s = 0; s < kMbThreads / 8; ++s)
         tc::mma_tf32(d2, tc::desc(sa2 + s * 2 * kMbLbo, kMbLbo, kMbSbo), tc::desc(sb2 + s * 2 * kMbLbo, kMbLbo, kMbSbo),
-                     id2, (it > 0 || s > 0) ? 1u : 0u);
+                     id2, (it % kMbFlush != 0 || s > 0) ? 1u : 0u);
       tc::commit(&bar2);
     }
     prev_out = valid ? (bb * cin * npts + p) : -1;
@@ -234,29 +265,24 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     tc::mbar_wait(&bar2, (it - 1) & 1);
     tc::fence_after();
     if (want_gin) drain_gin();
+    fold_d2();  // the last (possibly partial) chunk
   }
-  // ---- weight-gradient partial: D2 quadrants -> shared -> partial
+  // ---- weight-gradient partial: a_hi and a_lo rows of ACC -> shared -> partial
   __syncthreads();  // every thread is past its last operand write
-  float* st = reinterpret_cast<float*>(smem);  // [64][65], aliases A2 (all MMAs done)
+  float* st = reinterpret_cast<float*>(smem);  // [64][33], aliases A2 (all MMAs done)
   if (it > 0 && warp < 2) {
-    uint32_t r0[32], r1[32];
-    tc::tmem_ld32_nowait(d2 + lane_off, r0);
-    tc::tmem_ld32_nowait(d2 + lane_off + 32, r1);
+    uint32_t r0[32];
+    tc::tmem_ld32_nowait(dacc + lane_off, r0);
     tc::tmem_ld_wait();
     const int row = 32 * warp + lane;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      st[row * 65 + c] = __uint_as_float(r0[c]);
-      st[row * 65 + 32 + c] = __uint_as_float(r1[c]);
-    }
+    for (int c = 0; c < 32; ++c) st[row * 33 + c] = __uint_as_float(r0[c]);
   }
   __syncthreads();
   float* outp = partials + (long long)blockIdx.x * cin * cout;
   for (int e = tid; e < cin * cout; e += kMbThreads) {
     const int i = e / cout, o = e % cout;
-    float v = 0.f;
-    if (it > 0) v = (st[i * 65 + o] + st[i * 65 + 32 + o]) + (st[(32 + i) * 65 + o] + st[(32 + i) * 65 + 32 + o]);
-    outp[e] = v;
+    outp[e] = it > 0 ? st[i * 33 + o] + st[(32 + i) * 33 + o] : 0.f;
   }
   tc::fence_before();
   __syncthreads();
@@ -567,12 +593,14 @@ __global__ void __launch_bounds__(kMbThreads + 32, 4)
         const uint32_t id = tc::idesc_tf32(128, NPo);
         const uint32_t sb = tc::smem_u32(b1);
         const uint32_t d = dcol(it);
+        // lo products first, hi.hi last: the accumulator's non-round-to-nearest
+        // adds bias only the KPi / 8 full-magnitude sums
         for (int k = 0; k < KPi / 8; ++k) {
           const uint64_t bh = tc::desc(sb + k * 256, 128, sbo), bl = tc::desc(sb + plane + k * 256, 128, sbo);
-          tc::mma_tf32_ts(d, ah + 8 * k, bh, id, k > 0 ? 1u : 0u);
-          tc::mma_tf32_ts(d, al + 8 * k, bh, id, 1u);
+          tc::mma_tf32_ts(d, al + 8 * k, bh, id, k > 0 ? 1u : 0u);
           tc::mma_tf32_ts(d, ah + 8 * k, bl, id, 1u);
         }
+        for (int k = 0; k < KPi / 8; ++k) tc::mma_tf32_ts(d, ah + 8 * k, tc::desc(sb + k * 256, 128, sbo), id, 1u);
         tc::commit(&bar);
         if (nbuf == 2 && it >= 2) store(it - 2);  // staged by every worker before the barrier above
       }
