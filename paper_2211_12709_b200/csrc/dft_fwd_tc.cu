@@ -11,8 +11,15 @@
 // Per slab (b, c, x) the input [Ny][Nz][Nt] is walked in groups
 // (y chunk of 8, z block of 16) of 128 rows (y, z) x 32 t tiles:
 //
-//   TMA producer   4-D tensor-map loads (SWIZZLE_128B) of each tile into a
-//                  shared-memory ring (src, and pre in backward mode)
+//   producer       4-D tensor-map loads (SWIZZLE_128B) of each tile into a
+//                  shared-memory ring (src, and pre in backward mode).  TMA
+//                  needs 16-byte aligned row starts, so for N_t % 4 != 0 (the
+//                  CO2 grid's N_t = 86) two warps write the same swizzled
+//                  tiles with 8- or 4-byte cp.async instead, zero-filling
+//                  outside the grid (about half the TMA path's bandwidth)
+//   twiddle warp   builds the stage-Y operand of each y chunk (hi / lo planes,
+//                  K = 8 y re | im) from an fp64 phase table into a 2-slot
+//                  ring, so no N_y-sized table is resident
 //   converters     warps 0-3, thread = tile row (y, z): 8 conflict-free
 //                  LDS.128 of its 32 t, act / grad * act' fused, TF32 hi/lo
 //                  split, tcgen05.st into A_T (TMEM lane = row, column = t)
@@ -32,11 +39,12 @@
 // tests/test_gpu_tc_probe.py).  TMEM: 512 columns, one CTA per SM, persistent
 // over slabs.
 //
-// Envelope: fp32, r_y, r_z, r_t <= 16, Nt % 4 == 0 (TMA stride rule), 16-byte
-// aligned inputs; the caller falls back to dft_yzt_tc.cu otherwise.
+// Envelope: fp32, r_y, r_z, r_t <= 16, inputs aligned to their cp.async piece
+// (8 bytes for even N_t, 4 otherwise; 16 for the TMA path), and the resident
+// t / z twiddle tables plus a 2-stage ring within shared memory (N_z <= 128 at
+// N_t <= 96 in backward mode).
 #include <cuda.h>
-#include <stdio.h>
-#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -53,22 +61,25 @@ constexpr int kZepiW0 = 16;               // warps 16-19: D2 -> A_Y, D3 -> outpu
 constexpr int kTmaW = 20;                 // TMA producer
 constexpr int kIssT0 = 21, kIssT1 = 22;   // stage-T issuers (group parity when one t block per group)
 constexpr int kIssZ = 23, kIssY = 24;     // stage-Z / stage-Y issuers
-constexpr int kWarps = 25;
+constexpr int kTwW = 25;                  // stage-Y twiddle builder
+constexpr int kWarps = 26;
 constexpr int kThreads2 = kWarps * 32;
 constexpr int kTileBytes = 128 * 32 * 4;            // 128 rows x 32 t fp32
 constexpr int kScratchWarp = 2 * 16 * 17 * 4;       // [yy][kt][z (+1)], one part (re / im) at a time
 constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
 constexpr int kAYPlane = 16 * 512;                  // 128 rows x K 16, SBO 512 (one hi or lo plane of one tile)
 constexpr int kAYBytes = 4 * kAYPlane;              // 2 tiles x (hi, lo)
+constexpr int kBYPlane = 4 * 512;                   // 32 rows x K 16 (8 y re | im), SBO 512
+constexpr int kBYSlot = 2 * kBYPlane;               // hi, lo
 
 // TMEM column map (512): A_T 2x64 | D1 2x32 | A_Z 2x64 | D2 2x64 (hi.hi | hi.lo+lo.hi) | D3 2 tiles x 32
 constexpr uint32_t cAT = 0, cD1 = 128, cAZ = 192, cD2 = 320, cD3 = 448;
 
 struct Lay {
   int nyc, nzb, ntb;            // y chunks (8), z blocks (16), t blocks (32)
-  int kt_tot, kz_tot, ky_tot;   // K extents of the twiddle operands
-  int sbo_t, sbo_z, sbo_y;
-  int off_ring, off_bt, off_bz, off_by, off_scr, off_stash, off_ay, total;
+  int kt_tot, kz_tot;           // K extents of the resident twiddle operands
+  int sbo_t, sbo_z;
+  int off_ring, off_bt, off_bz, off_by, off_ph, off_scr, off_stash, off_ay, total;
   int stages, srcs;             // ring depth, tiles per stage (1 or 2)
 };
 
@@ -79,15 +90,14 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.ntb = (nt + 31) / 32;
   L.kt_tot = L.ntb * 32;
   L.kz_tot = L.nzb * 32;
-  L.ky_tot = L.nyc * 16;
   L.sbo_t = (L.kt_tot / 4) * 128;
   L.sbo_z = (L.kz_tot / 4) * 128;
-  L.sbo_y = (L.ky_tot / 4) * 128;
   L.srcs = srcs;
   int o = 0;
   L.off_bt = o; o += 2 * 4 * L.sbo_t;   // hi, lo planes of 32 rows
   L.off_bz = o; o += 2 * 4 * L.sbo_z;
-  L.off_by = o; o += 2 * 4 * L.sbo_y;
+  L.off_by = o; o += 2 * kBYSlot;       // 2-slot ring of per-chunk Y operands
+  L.off_ph = o; o += ((16 * ny + 127) / 128) * 128;  // e^{2 pi i j / N_y} as (cos hi, cos lo, sin hi, sin lo)
   L.off_scr = o; o += 8 * kScratchWarp;
   L.off_stash = o; o += kStashBytes;
   o = (o + 1023) & ~1023;
@@ -145,22 +155,14 @@ struct GroupIdx {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
-                  const __grid_constant__ CUtensorMap tm_pre, float scale, float2* __restrict__ out, int smem_cap,
-                  unsigned long long* __restrict__ prof, int pf_dist) {
+                  const __grid_constant__ CUtensorMap tm_pre, const float* __restrict__ srcp,
+                  const float* __restrict__ prep, int use_ca, float scale, float2* __restrict__ out, int smem_cap) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
-  // optional wait profile (debug): per warp, cycles waiting in slots 0..3 and total
-  long long wt[4] = {0, 0, 0, 0};
-  const long long t_start = clock64();
-#define DFNO_W(slot, call)                        \
-  do {                                            \
-    const long long t0_ = clock64();              \
-    call;                                         \
-    if (prof) wt[slot] += clock64() - t0_;         \
-  } while (0)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[4], empty[4], at_full[2], at_empty[2], d1_full[2], d1_empty[2];
   __shared__ uint64_t az_full[2], az_empty[2], d2_full[2], d2_empty[2], ay_full, ay_empty, d3_full, d3_empty;
+  __shared__ uint64_t by_full[2], by_empty[2];
   __shared__ uint32_t tmem_base;
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
   unsigned char* bz = smem + L.off_bz;
   unsigned char* by = smem + L.off_by;
   unsigned char* ay = smem + L.off_ay;
+  float4* ph = reinterpret_cast<float4*>(smem + L.off_ph);
 
   // ---- twiddle operands (hi / lo planes, K-major, 32 rows each) -----------
   {
@@ -193,20 +196,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
       cs(n & 15, z, Nz, g.mz, g.rz, c, s);
       put_split(bz, plz, kmaj32(n, k, L.sbo_z), (n < 16) ? (part ? s : c) : (part ? c : -s));
     }
-    const int ply = 4 * L.sbo_y;
-    for (int e = tid; e < 32 * L.ky_tot; e += blockDim.x) {
-      const int n = e / L.ky_tot, k = e % L.ky_tot;
-      const int y = (k / 16) * 8 + (k & 7), part = (k >> 3) & 1;
+    for (int j = tid; j < Ny; j += blockDim.x) {
       double c, s;
-      cs(n & 15, y, Ny, g.my, g.ry, c, s);
-      put_split(by, ply, kmaj32(n, k, L.sbo_y), (n < 16) ? (part ? s : c) : (part ? c : -s));
+      sincospi(2.0 * (double)j / Ny, &s, &c);
+      const float ch = tc::round_tf32((float)c), sh = tc::round_tf32((float)s);
+      ph[j] = make_float4(ch, tc::round_tf32((float)(c - (double)ch)), sh, tc::round_tf32((float)(s - (double)sh)));
     }
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int s = 0; s < 4; ++s) {
-      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&full[s], use_ca ? 64 : 1);  // cp.async: one arrival per producer lane (2 warps)
       tc::mbar_init(&empty[s], 128);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&by_full[b], 32);
+      tc::mbar_init(&by_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&at_full[b], 128);
@@ -240,6 +245,68 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const bool two_t = (L.ntb == 1);
   const uint32_t quarter_off = (uint32_t)(32 * (warp & 3)) << 16;
 
+  // cp.async producer (N_t % 4 != 0: no legal TMA row stride), run by two warps
+  // that split each tile's rows: row r = (y_l, z_l) of 32 t, 16-byte chunk c at
+  // c ^ (r & 7) (the TMA SWIZZLE_128B order the converters read), zero fill
+  // outside the grid.  `at_chunk(c)` runs when half 1 reaches y chunk c.
+  auto cp_async_producer = [&](int half, auto&& at_chunk) {
+    GroupIdx gi;
+    int tb = 0, chunk = 0;
+    const bool even = (Nt & 1) == 0;
+    const long long slab_elems = (long long)Ny * Nz * Nt;
+    for (int j = 0; j < n_tiles; ++j) {
+      if (tb == 0 && gi.zb == 0) at_chunk(chunk++);
+      const int s = j % S, n = j / S;
+      const long long slab = (long long)blockIdx.x + (long long)gi.slab_g * gridDim.x;
+      tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
+      unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
+#pragma unroll 1
+      for (int si = 0; si < L.srcs; ++si) {
+        const float* base = (si == 0 ? srcp : prep) + slab * slab_elems;
+        const uint32_t d0 = tc::smem_u32(dst + si * kTileBytes);
+        if (even) {
+          const int jj = lane & 15, rs = lane >> 4, t = tb * 32 + 2 * jj;
+          const bool tok = t < Nt;
+#pragma unroll 1
+          for (int yl = 4 * half; yl < 4 * half + 4; ++yl) {
+            const int y = gi.yc * 8 + yl;
+            const bool ok_y = tok && y < Ny;
+            const float* rowp = base + ((long long)y * Nz + gi.zb * 16) * Nt + t;
+#pragma unroll
+            for (int zz = 0; zz < 8; ++zz) {
+              const int zl = 2 * zz + rs, r = yl * 16 + zl;
+              const bool ok = ok_y && gi.zb * 16 + zl < Nz;
+              tc::cp_async8(d0 + r * 128 + ((((jj >> 1) ^ (zl & 7))) << 4) + (jj & 1) * 8,
+                            ok ? rowp + zl * Nt : base, ok ? 8u : 0u);
+            }
+          }
+        } else {
+          const int t = tb * 32 + lane;
+          const bool tok = t < Nt;
+#pragma unroll 1
+          for (int yl = 4 * half; yl < 4 * half + 4; ++yl) {
+            const int y = gi.yc * 8 + yl;
+            const bool ok_y = tok && y < Ny;
+            const float* rowp = base + ((long long)y * Nz + gi.zb * 16) * Nt + t;
+#pragma unroll 4
+            for (int zl = 0; zl < 16; ++zl) {
+              const int r = yl * 16 + zl;
+              const bool ok = ok_y && gi.zb * 16 + zl < Nz;
+              tc::cp_async4(d0 + r * 128 + (((lane >> 2) ^ (zl & 7)) << 4) + (lane & 3) * 4,
+                            ok ? rowp + zl * Nt : base, ok ? 4u : 0u);
+            }
+          }
+        }
+      }
+      tc::cp_async_mbar_arrive(&full[s]);
+      if (++tb == L.ntb) {
+        tb = 0;
+        gi.next(L);
+      }
+    }
+  };
+  auto no_chunk = [](int) {};
+
   if (warp < kConvW) {
     // ======================= converters =======================
     // two sets of 4 warps alternate tiles (measured faster than one set with a
@@ -249,7 +316,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int sw = r & 7;
     for (int i = set; set < kSets && i < n_tiles; i += kSets) {
       const int s = i % S, n = i / S;
-      DFNO_W(0, tc::mbar_wait_lazy(&full[s], n & 1, 32));
+      tc::mbar_wait_lazy(&full[s], n & 1, 32);
       const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
       const int b = i & 1;
 #pragma unroll
@@ -266,7 +333,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           tc::split_hl(conv<MODE, ACT>(q.z, p.z), h[4 * c4 + 2], l[4 * c4 + 2]);
           tc::split_hl(conv<MODE, ACT>(q.w, p.w), h[4 * c4 + 3], l[4 * c4 + 3]);
         }
-        if (half == 0) DFNO_W(1, tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1));
+        if (half == 0) tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
         tc::tmem_st16(tmem + cAT + 64 * b + 16 * half + quarter_off, h);
         tc::tmem_st16(tmem + cAT + 64 * b + 32 + 16 * half + quarter_off, l);
       }
@@ -282,14 +349,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int yy = lane >> 4, lo16 = lane & 15;
     for (int G = set; G < n_groups; G += 2) {
       const int b = G & 1;
-      DFNO_W(0, tc::mbar_wait(&d1_full[b], (G >> 1) & 1));
+      tc::mbar_wait(&d1_full[b], (G >> 1) & 1);
       tc::fence_after();
       uint32_t u[32];
       tc::tmem_ld32_nowait(tmem + cD1 + 32 * b + quarter_off, u);
       tc::tmem_ld_wait();
       tc::fence_before();
       tc::mbar_arrive(&d1_empty[b]);
-      DFNO_W(1, tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1));
+      tc::mbar_wait(&az_empty[b], ((G >> 1) & 1) ^ 1);
       tc::fence_after();
 #pragma unroll
       for (int part = 0; part < 2; ++part) {  // A_Z cols: hi re | hi im | lo re | lo im
@@ -316,7 +383,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     int slab_i = 0;
     for (int c = 0; c < n_chunks; ++c) {
       const int yc = c % L.nyc, cb = c & 1;
-      DFNO_W(0, tc::mbar_wait_lazy(&d2_full[cb], (c >> 1) & 1));
+      tc::mbar_wait_lazy(&d2_full[cb], (c >> 1) & 1);
       tc::fence_after();
       uint32_t u0[32];
       {
@@ -338,7 +405,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
       }
       tc::named_sync(1, 128);
-      DFNO_W(1, tc::mbar_wait_lazy(&ay_empty, (c & 1) ^ 1));
+      tc::mbar_wait_lazy(&ay_empty, (c & 1) ^ 1);
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         // A_Y tile hh row (kz_l, kt), K = (re y0..7, im y0..7), hi / lo planes,
@@ -365,7 +432,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       // ---- slab end: D3 -> XK exchange layout
       const int slab = (int)blockIdx.x + slab_i * (int)gridDim.x;
       const int xl = slab % XL, ch = (slab / XL) % g.c, bb = slab / (XL * g.c);
-      DFNO_W(2, tc::mbar_wait_lazy(&d3_full, slab_i & 1));
+      tc::mbar_wait_lazy(&d3_full, slab_i & 1);
       tc::fence_after();
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
@@ -385,37 +452,62 @@ __global__ void __launch_bounds__(kThreads2, 1)
       ++slab_i;
     }
   } else if (warp == kTmaW) {
-    // ======================= TMA producer =======================
-    if (lane == 0) {
-      tc::tma_prefetch_desc(&tm_src);
-      if (GRAD) tc::tma_prefetch_desc(&tm_pre);
-      GroupIdx gi, gp;  // gp runs kPf tiles ahead: L2 prefetch deepens the stream beyond the smem ring
-      int tb = 0, tbp = 0;
-      const int kPf = pf_dist;
-      for (int i = 0; i < n_tiles + kPf; ++i) {
-        if (i < n_tiles) {
-          const int slabp = (int)blockIdx.x + gp.slab_g * (int)gridDim.x;
-          tc::tma_prefetch_4d(&tm_src, tbp * 32, gp.zb * 16, gp.yc * 8, slabp);
-          if (GRAD) tc::tma_prefetch_4d(&tm_pre, tbp * 32, gp.zb * 16, gp.yc * 8, slabp);
-          if (++tbp == L.ntb) {
-            tbp = 0;
-            gp.next(L);
+    // ======================= producer =======================
+    if (!use_ca) {
+      if (lane == 0) {
+        tc::tma_prefetch_desc(&tm_src);
+        if (GRAD) tc::tma_prefetch_desc(&tm_pre);
+        GroupIdx gi;
+        int tb = 0;
+        for (int j = 0; j < n_tiles; ++j) {
+          const int s = j % S, n = j / S;
+          const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
+          tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
+          tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
+          unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
+          tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+          if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+          if (++tb == L.ntb) {
+            tb = 0;
+            gi.next(L);
           }
         }
-        if (i < kPf) continue;
-        const int j = i - kPf;
-        const int s = j % S, n = j / S;
-        const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
-        DFNO_W(0, tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64));
-        tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
-        unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
-        tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
-        if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
-        if (++tb == L.ntb) {
-          tb = 0;
-          gi.next(L);
-        }
       }
+    } else {
+      cp_async_producer(0, no_chunk);
+    }
+  } else if (warp == kTwW) {
+    // ======================= stage-Y twiddles (+ half the cp.async rows) =======================
+    // rows n: 0-15 out re (C on re, S on im), 16-31 out im (-S on re, C on im);
+    // K = (re y0..7, im y0..7) of the chunk; e^{-i}: value from the phase table
+    const int ky = lane & 15, y0 = 4 * (lane >> 4);
+    const bool ky_ok = ky < g.ry;
+    const int f = mode_freq(ky, Ny, g.my);
+    auto build = [&](int c) {
+      const int yc = c % L.nyc, b = c & 1;
+      tc::mbar_wait_lazy(&by_empty[b], ((c >> 1) & 1) ^ 1, 64);
+      float* hi = reinterpret_cast<float*>(by + b * kBYSlot);
+      float* lo = hi + kBYPlane / 4;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int yl = y0 + j, y = yc * 8 + yl;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ky_ok && y < Ny) v = ph[(f * y) % Ny];
+        // (row, K): (ky, y re) C | (ky, y im) S | (16 + ky, y re) -S | (16 + ky, y im) C
+        const int o00 = kmaj32(ky, yl, 512) / 4, o01 = kmaj32(ky, 8 + yl, 512) / 4;
+        const int o10 = kmaj32(16 + ky, yl, 512) / 4, o11 = kmaj32(16 + ky, 8 + yl, 512) / 4;
+        hi[o00] = v.x; lo[o00] = v.y;
+        hi[o01] = v.z; lo[o01] = v.w;
+        hi[o10] = -v.z; lo[o10] = -v.w;
+        hi[o11] = v.x; lo[o11] = v.y;
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&by_full[b]);
+    };
+    if (use_ca) {
+      cp_async_producer(1, build);
+    } else {
+      for (int c = 0; c < n_chunks; ++c) build(c);
     }
   } else if (warp == kIssT0 || warp == kIssT1) {
     // ======================= stage T issuers =======================
@@ -425,10 +517,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const uint32_t sbt = tc::smem_u32(bt), plt = 4 * L.sbo_t;
       for (int G = two_t ? k : 0; G < n_groups; G += two_t ? 2 : 1) {
         const int b = G & 1;
-        DFNO_W(0, tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1));
+        tc::mbar_wait(&d1_empty[b], ((G >> 1) & 1) ^ 1);
         for (int tb = 0; tb < L.ntb; ++tb) {
           const int i = G * L.ntb + tb, ab = i & 1;
-          DFNO_W(1, tc::mbar_wait(&at_full[ab], (i >> 1) & 1));
+          tc::mbar_wait(&at_full[ab], (i >> 1) & 1);
           tc::fence_after();
           const uint32_t a = tmem + cAT + 64 * ab, d = tmem + cD1 + 32 * b;
           // lo products first, hi.hi last: the accumulator's adds are not
@@ -458,8 +550,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
       int chunk = 0;
       for (int G = 0; G < n_groups; ++G) {
         const int b = G & 1, cb = chunk & 1;
-        DFNO_W(0, tc::mbar_wait(&az_full[b], (G >> 1) & 1));
-        if (gi.zb == 0) DFNO_W(1, tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1));
+        tc::mbar_wait(&az_full[b], (G >> 1) & 1);
+        if (gi.zb == 0) tc::mbar_wait(&d2_empty[cb], ((chunk >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t a = tmem + cAZ + 64 * b, d = tmem + cD2 + 64 * cb;
 #pragma unroll
@@ -480,12 +572,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
     // ======================= stage Y issuer (A_Y in shared memory) =======================
     if (lane == 0) {
       const uint32_t id = tc::idesc_tf32(128, 32);
-      const uint32_t sby = tc::smem_u32(by), ply = 4 * L.sbo_y, say = tc::smem_u32(ay);
+      const uint32_t say = tc::smem_u32(ay);
       int slab_i = 0;
       for (int c = 0; c < n_chunks; ++c) {
-        const int yc = c % L.nyc;
-        DFNO_W(0, tc::mbar_wait_lazy(&ay_full, c & 1, 64));
-        if (yc == 0) DFNO_W(1, tc::mbar_wait_lazy(&d3_empty, (slab_i & 1) ^ 1, 64));
+        const int yc = c % L.nyc, bb = c & 1;
+        const uint32_t sby = tc::smem_u32(by + bb * kBYSlot);
+        tc::mbar_wait_lazy(&ay_full, c & 1, 64);
+        tc::mbar_wait_lazy(&by_full[bb], (c >> 1) & 1, 32);
+        if (yc == 0) tc::mbar_wait_lazy(&d3_empty, (slab_i & 1) ^ 1, 64);
         tc::fence_after();
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -493,8 +587,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
           const uint32_t a_hi = say + (2 * hh) * kAYPlane, a_lo = a_hi + kAYPlane;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            const uint32_t kb = (uint32_t)(yc * 2 + s) * 256;
-            const uint64_t bh = tc::desc(sby + kb, 128, L.sbo_y), bl = tc::desc(sby + ply + kb, 128, L.sbo_y);
+            const uint32_t kb = (uint32_t)s * 256;
+            const uint64_t bh = tc::desc(sby + kb, 128, 512), bl = tc::desc(sby + kBYPlane + kb, 128, 512);
             const uint64_t ah = tc::desc(a_hi + s * 256, 128, 512), al = tc::desc(a_lo + s * 256, 128, 512);
             tc::mma_tf32(d, ah, bh, id, (yc | s) ? 1u : 0u);
             tc::mma_tf32(d, al, bh, id, 1u);
@@ -502,6 +596,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           }
         }
         tc::commit(&ay_empty);
+        tc::commit(&by_empty[bb]);
         if (yc == L.nyc - 1) {
           tc::commit(&d3_full);
           ++slab_i;
@@ -509,15 +604,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
       }
     }
   }
-  if (prof && lane == 0) {
-    const long long tot = clock64() - t_start;
-    atomicAdd(prof + warp * 5 + 0, (unsigned long long)wt[0]);
-    atomicAdd(prof + warp * 5 + 1, (unsigned long long)wt[1]);
-    atomicAdd(prof + warp * 5 + 2, (unsigned long long)wt[2]);
-    atomicAdd(prof + warp * 5 + 3, (unsigned long long)wt[3]);
-    atomicAdd(prof + warp * 5 + 4, (unsigned long long)tot);
-  }
-#undef DFNO_W
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -558,35 +644,24 @@ int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, 
   if (L.stages < 2) return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   CUtensorMap ms, mp;
-  if (!make_slab_map(&ms, src, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) return DFNO_ERR_UNSUPPORTED;
-  if (MODE == DFNO_SRC_GRAD) {
-    if (!make_slab_map(&mp, pre, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) return DFNO_ERR_UNSUPPORTED;
-  } else {
-    mp = ms;
+  // TMA when the t rows start on 16-byte boundaries, cp.async otherwise
+  bool tma = g.nt % 4 == 0 && !((uintptr_t)src & 15) && !(pre && ((uintptr_t)pre & 15)) &&
+             make_slab_map(&ms, src, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (tma && MODE == DFNO_SRC_GRAD)
+    tma = make_slab_map(&mp, pre, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (!tma) {
+    const uintptr_t piece = (g.nt % 2 == 0) ? 7 : 3;
+    if (((uintptr_t)src & piece) || (pre && ((uintptr_t)pre & piece))) return DFNO_ERR_UNSUPPORTED;
+    memset(&ms, 0, sizeof(ms));
   }
+  if (MODE != DFNO_SRC_GRAD || !tma) mp = ms;
   auto kern = k_yzt_fwd_tc2<MODE, ACT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int grid = sm_count2() < slabs ? sm_count2() : slabs;
-  static unsigned long long* prof = nullptr;
-  static const bool want_prof = getenv("DFNO_WAIT_PROFILE") && getenv("DFNO_WAIT_PROFILE")[0] == '1';
-  if (want_prof && !prof) cudaMalloc(&prof, kWarps * 5 * sizeof(unsigned long long));
-  if (prof) cudaMemsetAsync(prof, 0, kWarps * 5 * sizeof(unsigned long long), st);
-  // L2 prefetch distance in tiles (DFNO_YZT_PF overrides, for sweeps)
-  static const int pf_env = getenv("DFNO_YZT_PF") ? atoi(getenv("DFNO_YZT_PF")) : -1;
-  const int pf = pf_env >= 0 ? pf_env : 0;  // measured: prefetching slows the 2-input backward mode
-  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (float)scale, (float2*)out, cap, prof, pf);
+  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (const float*)src, (const float*)pre, tma ? 0 : 1,
+                                                (float)scale, (float2*)out, cap);
   DFNO_CUDA_CHECK_LAUNCH();
-  if (prof) {  // debug: per-warp wait cycles summed over CTAs
-    unsigned long long h[kWarps * 5];
-    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    fprintf(stderr, "yzt_fwd_tc2 mode %d: per-CTA avg cycles  [w0 w1 w2 w3 | total]\n", MODE);
-    for (int w = 0; w < kWarps; ++w)
-      fprintf(stderr, "  warp %2d: %9.0f %9.0f %9.0f %9.0f | %9.0f\n", w, h[w * 5] / (double)grid,
-              h[w * 5 + 1] / (double)grid, h[w * 5 + 2] / (double)grid, h[w * 5 + 3] / (double)grid,
-              h[w * 5 + 4] / (double)grid);
-  }
   return DFNO_OK;
 }
 
@@ -604,7 +679,6 @@ int launch2_act(const dfno_geom& g, const void* src, const void* pre, double sca
 int yzt_fwd_tc2(const dfno_geom& g, const void* src, const void* pre, int mode, double scale, void* out,
                 cudaStream_t st) {
   if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;
-  if (g.nt % 4 != 0 || ((uintptr_t)src & 15) || (pre && ((uintptr_t)pre & 15))) return DFNO_ERR_UNSUPPORTED;
   switch (mode) {
     case DFNO_SRC_ACT: return launch2_act<DFNO_SRC_ACT>(g, src, pre, scale, out, st);
     case DFNO_SRC_GRAD: return launch2_act<DFNO_SRC_GRAD>(g, src, pre, scale, out, st);

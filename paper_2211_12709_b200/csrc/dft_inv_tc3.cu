@@ -2,36 +2,39 @@
 // tcgen05 tensor cores (kind::tf32, 3xTF32), stage order Y' -> T' -> Z'.
 //
 // Replaces pad_modes + ifft_dims(yzt) + .real (reference d/fno.py:338-343,
-// scale 1/N_yzt) and its backward use (d/fno.py:459-464, scale 1), like
-// dft_inv_tc.cu, whose Y' -> Z' -> T' order ends on a real N = N_t = 32 stage
-// with 32 output tiles per slab and a per-tile (kt <-> z) transpose.  Here the
-// last stage contracts kz with the real z output as the MMA N (= 64): half the
-// output tiles, twice the N per MMA, and the accumulator rows (y, t) are
-// already the output's contiguous dimension, so the output epilogue stores
-// straight from TMEM with coalesced 128-byte rows -- no transposes.
+// scale 1/N_yzt) and its backward use (d/fno.py:459-464, scale 1).  The last
+// stage contracts kz with the real z output as the MMA N (= 64 per z block),
+// so the accumulator rows (y, t) are already the output's contiguous
+// dimension and the output epilogue stores straight from TMEM with coalesced
+// 128-byte t rows -- no transposes, no alignment rule on the output grid.
 //
 // Per slab (b, c, x):
-//   loader  warp 20: V (16 contiguous (kz, kt) blocks per slab) -> shared, bulk
-//           copies one slab ahead
-//   front   warps 0-3: V -> A_Y (shared), rows (kz, kt) [2 tiles], K = (ky re | ky im)
-//   MMA Y'  D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (SS, N=32,
-//           16 y per pass)
-//   front   D_Y -> stash1 -> A_T[(y 8, kz)][(kt re | kt im)] (TMEM) per 8-y chunk
-//   MMA T'  D_T[(y,kz)][t re 32 | t im 32] = A_T . [[C,-S];[S,C]]_t  (TS, N=64)
-//   T epi   warps 4-7: D_T -> stash2 -> A_Z[(y 4, t)][(kz re | kz im)] (TMEM),
-//           two Z' tiles per T' tile
-//   MMA Z'  D_Z[(y,t)][z] = Re(A_Z . e^{+i kz z}) = A_Z . [C ; -S]_z  (TS, N=64;
-//           two issuers by tile parity)
-//   O epi   warps 8-15 (two sets by tile parity): D_Z -> global, one 128-byte
-//           t row per (warp, z) (the output scale is folded into B_Z)
+//   loader   warp 20: V (16 contiguous (kz, kt) blocks per slab) -> shared, bulk
+//            copies one slab ahead
+//   twiddle  warp 21: the Y' operand of each 16-y pass (hi / lo planes) from a
+//            phase table into a one-slot buffer, so no N_y-sized table is
+//            resident
+//   front    warps 0-3: V -> A_Y (shared), rows (kz, kt) [2 tiles], K = (ky re | ky im)
+//   MMA Y'   D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (SS, N=32,
+//            16 y per pass)
+//   front    D_Y -> stash1 -> A_T[(y 8, kz)][(kt re | kt im)] (TMEM) per 8-y chunk
+//   MMA T'   per 32-t block tb: D_T[(y,kz)][t re 32 | t im 32] = A_T . [[C,-S];[S,C]]_t
+//            (TS, N=64)
+//   T epi    warps 4-7: D_T -> stash2 -> A_Z[(y 4, t)][(kz re | kz im)] (TMEM),
+//            two Z' tiles per (chunk, t block)
+//   MMA Z'   per 64-z block: D_Z[(y,t)][z] = Re(A_Z . e^{+i kz z}) = A_Z . [C ; -S]_z
+//            (TS, N=64; two issuers by tile parity)
+//   O epi    warps 8-15 (two sets by tile parity): D_Z -> global, one 128-byte
+//            t row per (warp, z) (the output scale is folded into B_Z)
 // All hand-offs are mbarrier full / empty pairs; TMEM 512 columns, one CTA per
-// SM, persistent over slabs.
+// SM, persistent over slabs.  Every accumulation issues its small lo products
+// before the hi.hi products: the accumulator's adds are not round-to-nearest,
+// so only the hi.hi sums should meet a full-magnitude accumulator (DESIGN.md
+// section 3).
 //
-// Envelope: fp32, r_y, r_z, r_t <= 16, N_z <= 64, N_t <= 32 (the caller falls
-// back to dft_inv_tc.cu otherwise).
-#include <stdio.h>
-#include <stdlib.h>
-
+// Envelope: fp32, r_y, r_z, r_t <= 16, r_z r_t even, 16-byte aligned input,
+// and the resident t / z twiddles (16 KB per 32-t / 64-z block) within shared
+// memory (e.g. the CO2 grid's N_t = 86 with N_z = 64, or N_z = 128 with N_t = 32).
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -42,10 +45,12 @@ namespace {
 constexpr int wTepi3 = 4;    // warps 4-7
 constexpr int wOepi3 = 8;    // warps 8-15, set = (warp - 8) / 4
 constexpr int wIssY3 = 16, wIssT3 = 17, wIssZ3 = 18;  // Z': 18, 19
-constexpr int wLoad3 = 20;
-constexpr int kWarps3 = 21;
+constexpr int wLoad3 = 20, wTw3 = 21;
+constexpr int kWarps3 = 22;
 constexpr int kThreads3 = kWarps3 * 32;
 constexpr int kAYPlane3 = 16 * 1024;          // 128 rows x K 32 fp32
+constexpr int kBYPlane3 = 4 * 1024;           // one pass: 32 rows (re | im, y 16) x K 32
+constexpr int kBlk3 = 16 * 1024;              // one t or z block of twiddles: 64 rows x K 32, hi + lo
 constexpr int kS1 = 20;                       // stash1 kt pitch (floats)
 constexpr int kS2 = 65;                       // stash2 row pitch (floats)
 
@@ -53,21 +58,22 @@ constexpr int kS2 = 65;                       // stash2 row pitch (floats)
 constexpr uint32_t jDY = 0, jAT = 64, jDT = 128, jAZ = 256, jDZ = 384;
 
 struct Lay3 {
-  int npass, nyc;
-  int off_ay, off_by, off_bt, off_bz, off_s1, off_s2, off_v, total;
-  int by_plane;
+  int npass, nyc, ntb, nzo;
+  int off_ay, off_by, off_bt, off_bz, off_ph, off_s1, off_s2, off_v, total;
 };
 
-__host__ __device__ inline Lay3 make_lay3(int ny) {
+__host__ __device__ inline Lay3 make_lay3(int ny, int nz, int nt) {
   Lay3 L;
   L.npass = (ny + 15) / 16;
   L.nyc = (ny + 7) / 8;
-  L.by_plane = L.npass * 32 / 8 * 1024;  // rows (pass, re|im, y 16) x K 32
+  L.ntb = (nt + 31) / 32;
+  L.nzo = (nz + 63) / 64;
   int o = 0;
   L.off_ay = o; o += 4 * kAYPlane3;      // tile 0 hi, tile 0 lo, tile 1 hi, tile 1 lo
-  L.off_by = o; o += 2 * L.by_plane;
-  L.off_bt = o; o += 2 * 8 * 1024;       // rows t re 32 | t im 32
-  L.off_bz = o; o += 2 * 8 * 1024;       // rows z 64
+  L.off_by = o; o += 2 * kBYPlane3;      // one pass, hi | lo
+  L.off_bt = o; o += L.ntb * kBlk3;      // per t block: rows t re 32 | t im 32, hi | lo
+  L.off_bz = o; o += L.nzo * kBlk3;      // per z block: rows z 64, hi | lo
+  L.off_ph = o; o += ((16 * ny + 1023) / 1024) * 1024;  // e^{2 pi i j / N_y}: cos hi, cos lo, sin hi, sin lo
   L.off_s1 = o; o += 2 * 8 * 16 * kS1 * 4;
   L.off_s2 = o; o += ((8 * 16 * kS2 * 4 + 1023) / 1024) * 1024;
   L.off_v = o; o += 16 * 256 * 8;        // a slab's modes [ky][kz][kt] complex (r_z r_t per ky)
@@ -102,55 +108,45 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
 
 template <bool FAST>  // FAST: N_z == 64 and N_t == 32 (compile-time store offsets)
 __global__ void __launch_bounds__(kThreads3, 1)
-    k_yzt_inv_tc3(const dfno_geom g, const float2* __restrict__ in, float* __restrict__ out, float scale,
-                  unsigned long long* __restrict__ prof) {
-  long long wt[4] = {0, 0, 0, 0};
-  const long long t_start = clock64();
-#define DFNO_W(slot, call)                \
-  do {                                    \
-    const long long t0_ = clock64();      \
-    call;                                 \
-    if (prof) wt[slot] += clock64() - t0_; \
-  } while (0)
+    k_yzt_inv_tc3(const dfno_geom g, const float2* __restrict__ in, float* __restrict__ out, float scale) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t v_full, v_empty, ay_full, ay_empty, dy_full, dy_empty, at_full, at_empty;
+  __shared__ uint64_t v_full, v_empty, ay_full, ay_empty, dy_full, dy_empty, at_full, at_empty, by_full, by_empty;
   __shared__ uint64_t dt_full[2], dt_empty[2], az_full[2], az_empty[2], dz_full[2], dz_empty[2];
   __shared__ uint32_t tmem_base;
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
-  const Lay3 L = make_lay3(Ny);
+  const Lay3 L = make_lay3(Ny, Nz, Nt);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* ay = smem + L.off_ay;
   unsigned char* by = smem + L.off_by;
   unsigned char* bt = smem + L.off_bt;
   unsigned char* bz = smem + L.off_bz;
+  float4* ph = reinterpret_cast<float4*>(smem + L.off_ph);
 
-  // ---- twiddles (hi / lo planes, K-major) -----------------------------------
-  // B_Y rows (pass, re|im, y 16), K = (ky re | ky im): e^{+i ky y}
-  for (int e = tid; e < L.npass * 32 * 32; e += blockDim.x) {
-    const int n = e / 32, k = e % 32;
-    const int y = (n / 32) * 16 + (n & 15), out_im = (n >> 4) & 1, in_im = k >> 4;
-    double c, s;
-    csi3(k & 15, y, Ny, g.my, g.ry, c, s);
-    put_split3(by, L.by_plane, kmaj3(n, k), out_im ? (in_im ? c : s) : (in_im ? -s : c));
-  }
-  // B_T rows (t re 32 | t im 32), K = (kt re | kt im)
-  for (int e = tid; e < 64 * 32; e += blockDim.x) {
-    const int n = e / 32, k = e % 32;
-    const int t = n & 31, out_im = n >> 5, in_im = k >> 4;
+  // ---- resident twiddles (hi / lo planes, K-major) and the y phase table ----
+  // B_T block tb: rows (t re 32 | t im 32), K = (kt re | kt im), t = 32 tb + row
+  for (int e = tid; e < L.ntb * 64 * 32; e += blockDim.x) {
+    const int tb = e / 2048, n = (e / 32) & 63, k = e % 32;
+    const int t = 32 * tb + (n & 31), out_im = n >> 5, in_im = k >> 4;
     double c, s;
     csi3(k & 15, t, Nt, g.mt, g.rt, c, s);
-    put_split3(bt, 8 * 1024, kmaj3(n, k), out_im ? (in_im ? c : s) : (in_im ? -s : c));
+    put_split3(bt + tb * kBlk3, 8 * 1024, kmaj3(n, k), out_im ? (in_im ? c : s) : (in_im ? -s : c));
   }
-  // B_Z rows z 64, K = (kz re | kz im): Re(A e^{+i kz z}) = Are C - Aim S; the
-  // output scale is folded in (exact for the power-of-two 1 / N_yzt)
-  for (int e = tid; e < 64 * 32; e += blockDim.x) {
-    const int z = e / 32, k = e % 32, in_im = k >> 4;
+  // B_Z block zo: rows z 64, K = (kz re | kz im): Re(A e^{+i kz z}) = Are C - Aim S;
+  // the output scale is folded in (exact for the power-of-two 1 / N_yzt)
+  for (int e = tid; e < L.nzo * 64 * 32; e += blockDim.x) {
+    const int zo = e / 2048, n = (e / 32) & 63, k = e % 32, in_im = k >> 4;
     double c, s;
-    csi3(k & 15, z, Nz, g.mz, g.rz, c, s);
-    put_split3(bz, 8 * 1024, kmaj3(z, k), (double)scale * (in_im ? -s : c));
+    csi3(k & 15, 64 * zo + n, Nz, g.mz, g.rz, c, s);
+    put_split3(bz + zo * kBlk3, 8 * 1024, kmaj3(n, k), (double)scale * (in_im ? -s : c));
+  }
+  for (int j = tid; j < Ny; j += blockDim.x) {
+    double c, s;
+    sincospi(2.0 * (double)j / Ny, &s, &c);
+    const float ch = tc::round_tf32((float)c), sh = tc::round_tf32((float)s);
+    ph[j] = make_float4(ch, tc::round_tf32((float)(c - (double)ch)), sh, tc::round_tf32((float)(s - (double)sh)));
   }
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
@@ -162,6 +158,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
     tc::mbar_init(&dy_empty, 128);
     tc::mbar_init(&at_full, 128);
     tc::mbar_init(&at_empty, 1);
+    tc::mbar_init(&by_full, 32);
+    tc::mbar_init(&by_empty, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&dt_full[b], 1);
       tc::mbar_init(&dt_empty[b], 128);
@@ -181,8 +179,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
 
   const int slabs = g.batch * g.c * XL;
   const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int n_chunks = my_slabs * L.nyc;  // T' tiles (8 y)
-  const int n_ztiles = 2 * n_chunks;      // Z' tiles (4 y)
+  const int n_chunks = my_slabs * L.nyc;  // A_T tiles (8 y)
+  const int n_units = n_chunks * L.ntb;   // T' tiles (8 y, 32 t)
+  const int n_ztiles = 2 * n_units;       // Z' tiles (4 y, 32 t)
 
   if (warp < wTepi3) {
     // ======================= front: V -> A_Y ; D_Y -> A_T =======================
@@ -192,8 +191,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const float2* vs = reinterpret_cast<const float2*>(smem + L.off_v);
     const int rzt = g.rz * g.rt;
     for (int si = 0; si < my_slabs; ++si) {
-      DFNO_W(0, tc::mbar_wait_lazy(&ay_empty, (si & 1) ^ 1, 64));
-      DFNO_W(0, tc::mbar_wait(&v_full, si & 1));
+      tc::mbar_wait_lazy(&ay_empty, (si & 1) ^ 1, 64);
+      tc::mbar_wait(&v_full, si & 1);
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         float re[16], im[16];
@@ -206,8 +205,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
           re[ky] = v.x;
           im[ky] = v.y;
         }
-        unsigned char* ph = ay + (2 * hh) * kAYPlane3 + (row >> 3) * 1024 + (row & 7) * 16;
-        unsigned char* pl = ph + kAYPlane3;
+        unsigned char* phi = ay + (2 * hh) * kAYPlane3 + (row >> 3) * 1024 + (row & 7) * 16;
+        unsigned char* plo = phi + kAYPlane3;
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
           float h4[4], l4[4];
@@ -216,15 +215,15 @@ __global__ void __launch_bounds__(kThreads3, 1)
             const int k = 4 * k4 + j;
             tc::split_rn(k < 16 ? re[k] : im[k - 16], h4[j], l4[j]);
           }
-          *reinterpret_cast<float4*>(ph + k4 * 128) = make_float4(h4[0], h4[1], h4[2], h4[3]);
-          *reinterpret_cast<float4*>(pl + k4 * 128) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+          *reinterpret_cast<float4*>(phi + k4 * 128) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+          *reinterpret_cast<float4*>(plo + k4 * 128) = make_float4(l4[0], l4[1], l4[2], l4[3]);
         }
       }
       tc::mbar_arrive(&v_empty);
       tc::fence_proxy_async();
       tc::mbar_arrive(&ay_full);
       for (int p = 0; p < L.npass; ++p, ++pass_i) {
-        DFNO_W(1, tc::mbar_wait(&dy_full, pass_i & 1));
+        tc::mbar_wait(&dy_full, pass_i & 1);
         tc::fence_after();
         const int nchunk = min(2, L.nyc - 2 * p);
         for (int j = 0; j < nchunk; ++j, ++chunk) {
@@ -249,8 +248,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
               s1[((1 * 8 + y) * 16 + kz) * kS1 + kt] = __uint_as_float(u[2 * hh + 1][y]);
             }
           }
-          DFNO_W(3, tc::named_sync(1, 128));
-          DFNO_W(2, tc::mbar_wait(&at_empty, (chunk & 1) ^ 1));
+          tc::named_sync(1, 128);
+          tc::mbar_wait(&at_empty, (chunk & 1) ^ 1);
           tc::fence_after();
           {
             const int yl = 2 * q + (lane >> 4), kz = lane & 15;  // A_T row (y_l, kz)
@@ -273,18 +272,18 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::tmem_st_wait();
           tc::fence_before();
           tc::mbar_arrive(&at_full);
-          DFNO_W(3, tc::named_sync(1, 128));  // s1 consumed
+          tc::named_sync(1, 128);  // s1 consumed
         }
       }
     }
   } else if (warp < wOepi3) {
-    // ======================= T epilogue: D_T -> A_Z (two Z' tiles) =======================
+    // ======================= T epilogue: D_T -> A_Z (two Z' tiles per unit) =======================
     const int q = warp - wTepi3;
     float* s2 = reinterpret_cast<float*>(smem + L.off_s2);  // [y 8][kz 16][c 64 (t re | t im)], pitch kS2
     const int yl = 2 * q + (lane >> 4), kz = lane & 15;      // D_T row
-    for (int i = 0; i < n_chunks; ++i) {
+    for (int i = 0; i < n_units; ++i) {
       const int b = i & 1;
-      DFNO_W(0, tc::mbar_wait(&dt_full[b], (i >> 1) & 1));
+      tc::mbar_wait(&dt_full[b], (i >> 1) & 1);
       tc::fence_after();
       uint32_t u[64];
       {
@@ -299,17 +298,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
       float* dst = s2 + (yl * 16 + kz) * kS2;
 #pragma unroll
       for (int c = 0; c < 64; ++c) dst[c] = __uint_as_float(u[c]);
-      DFNO_W(3, tc::named_sync(2, 128));
+      tc::named_sync(2, 128);
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         const int zi = 2 * i + h, ab = zi & 1;
-        DFNO_W(1, tc::mbar_wait(&az_empty[ab], ((zi >> 1) & 1) ^ 1));
+        tc::mbar_wait(&az_empty[ab], ((zi >> 1) & 1) ^ 1);
         tc::fence_after();
         const float* src = s2 + ((4 * h + q) * 16) * kS2 + lane;  // A_Z row (y_l = 4h + q, t = lane)
         float hr[32], lr[32];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          tc::split_hl(src[k * kS2], hr[k], lr[k]);             // kz re
+          tc::split_hl(src[k * kS2], hr[k], lr[k]);                 // kz re
           tc::split_hl(src[k * kS2 + 32], hr[16 + k], lr[16 + k]);  // kz im
         }
         tc::tmem_st32(tmem + jAZ + 64 * ab + qoff, hr);
@@ -318,38 +317,47 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::fence_before();
         tc::mbar_arrive(&az_full[ab]);
       }
-      DFNO_W(3, tc::named_sync(2, 128));  // s2 consumed
+      tc::named_sync(2, 128);  // s2 consumed
     }
   } else if (warp < wIssY3) {
     // ======================= O epilogue: D_Z -> global =======================
-    const int k = (warp - wOepi3) >> 2, yq = warp & 3, t = lane;
+    const int k = (warp - wOepi3) >> 2, yq = warp & 3;
     const long long plane = (long long)Nz * Nt;
+    int v = 0;  // D_Z[k] fill count
     for (int zi = k; zi < n_ztiles; zi += 2) {
-      DFNO_W(0, tc::mbar_wait(&dz_full[k], (zi >> 1) & 1));
-      tc::fence_after();
-      uint32_t u[64];
-      {
-        uint32_t (&u0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&u[0]);
-        uint32_t (&u1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&u[32]);
-        tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + qoff, u0);
-        tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + 32 + qoff, u1);
-      }
-      tc::tmem_ld_wait();
-      tc::fence_before();
-      tc::mbar_arrive(&dz_empty[k]);
-      const int si = zi / (2 * L.nyc), yt = zi % (2 * L.nyc);
+      const int u = zi >> 1, h = zi & 1;
+      const int i = u / L.ntb, tb = u - i * L.ntb;
+      const int si = i / L.nyc, yc = i - si * L.nyc;
       const int slab = (int)blockIdx.x + si * (int)gridDim.x;
-      const int y = 4 * yt + yq;
+      const int y = 8 * yc + 4 * h + yq, t = 32 * tb + lane;
       float* o = out + ((long long)slab * Ny + y) * plane + t;
-      if (FAST) {
-        if (y < Ny) {
-#pragma unroll
-          for (int z = 0; z < 64; ++z) __stcs(o + z * 32, __uint_as_float(u[z]));
+      for (int zo = 0; zo < L.nzo; ++zo, ++v) {
+        tc::mbar_wait(&dz_full[k], v & 1);
+        tc::fence_after();
+        uint32_t w[64];
+        {
+          uint32_t (&u0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&w[0]);
+          uint32_t (&u1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&w[32]);
+          tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + qoff, u0);
+          tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + 32 + qoff, u1);
         }
-      } else if (y < Ny && t < Nt) {
+        tc::tmem_ld_wait();
+        tc::fence_before();
+        tc::mbar_arrive(&dz_empty[k]);
+        if (FAST) {
+          if (y < Ny) {
 #pragma unroll
-        for (int z = 0; z < 64; ++z)
-          if (z < Nz) __stcs(o + (long long)z * Nt, __uint_as_float(u[z]));
+            for (int z = 0; z < 64; ++z) __stcs(o + z * 32, __uint_as_float(w[z]));
+          }
+        } else if (y < Ny && t < Nt) {
+          float* oz = o + (long long)(64 * zo) * Nt;
+          const int zn = min(64, Nz - 64 * zo);
+#pragma unroll
+          for (int z = 0; z < 64; ++z) {
+            if (z < zn) __stcs(oz, __uint_as_float(w[z]));
+            oz += Nt;
+          }
+        }
       }
     }
   } else if (warp == wIssY3) {
@@ -359,59 +367,58 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const uint32_t say = tc::smem_u32(ay), sby = tc::smem_u32(by);
       int pass_i = 0;
       for (int si = 0; si < my_slabs; ++si) {
-        DFNO_W(0, tc::mbar_wait_lazy(&ay_full, si & 1, 64));
+        tc::mbar_wait_lazy(&ay_full, si & 1, 64);
         for (int p = 0; p < L.npass; ++p, ++pass_i) {
-          DFNO_W(1, tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1));
+          tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1);
+          tc::mbar_wait(&by_full, pass_i & 1);
           tc::fence_after();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const uint32_t d = tmem + jDY + 32 * hh;
             const uint32_t ah0 = say + (2 * hh) * kAYPlane3, al0 = ah0 + kAYPlane3;
-            // the small lo products first, the hi.hi products last: the
-            // accumulator's non-round-to-nearest adds then bias only the
-            // last four sums at full magnitude
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
+            for (int s = 0; s < 4; ++s) {  // lo products first
               const uint32_t kb = (uint32_t)s * 256;
-              const uint64_t ah = tc::desc(ah0 + kb, 128, 1024), al = tc::desc(al0 + kb, 128, 1024);
-              const uint64_t bh = tc::desc(sby + (uint32_t)p * 4096 + kb, 128, 1024);
-              const uint64_t bl = tc::desc(sby + L.by_plane + (uint32_t)p * 4096 + kb, 128, 1024);
-              tc::mma_tf32(d, al, bh, id, s ? 1u : 0u);
-              tc::mma_tf32(d, ah, bl, id, 1u);
+              tc::mma_tf32(d, tc::desc(al0 + kb, 128, 1024), tc::desc(sby + kb, 128, 1024), id, s ? 1u : 0u);
+              tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + kBYPlane3 + kb, 128, 1024), id, 1u);
             }
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
+            for (int s = 0; s < 4; ++s) {  // hi.hi last
               const uint32_t kb = (uint32_t)s * 256;
-              tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + (uint32_t)p * 4096 + kb, 128, 1024), id,
-                           1u);
+              tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + kb, 128, 1024), id, 1u);
             }
           }
+          tc::commit(&by_empty);
           tc::commit(&dy_full);
         }
         tc::commit(&ay_empty);
       }
     }
   } else if (warp == wIssT3) {
-    // ======================= MMA T' (TS, N = 64) =======================
+    // ======================= MMA T' (TS, N = 64), one unit per 32-t block =======================
     if (lane == 0) {
       const uint32_t id = tc::idesc_tf32(128, 64);
-      const uint32_t sbt = tc::smem_u32(bt);
+      const uint32_t sbt0 = tc::smem_u32(bt);
+      int u = 0;
       for (int i = 0; i < n_chunks; ++i) {
-        const int b = i & 1;
-        DFNO_W(0, tc::mbar_wait(&at_full, i & 1));
-        DFNO_W(1, tc::mbar_wait(&dt_empty[b], ((i >> 1) & 1) ^ 1));
+        tc::mbar_wait(&at_full, i & 1);
         tc::fence_after();
-        const uint32_t a = tmem + jAT, d = tmem + jDT + 64 * b;
+        const uint32_t a = tmem + jAT;
+        for (int tb = 0; tb < L.ntb; ++tb, ++u) {
+          const int b = u & 1;
+          tc::mbar_wait(&dt_empty[b], ((u >> 1) & 1) ^ 1);
+          tc::fence_after();
+          const uint32_t d = tmem + jDT + 64 * b, sbt = sbt0 + tb * kBlk3;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {  // lo products first, hi.hi last (see the Y' issuer)
-          const uint32_t kb = (uint32_t)s * 256;
-          const uint64_t bh = tc::desc(sbt + kb, 128, 1024), bl = tc::desc(sbt + 8 * 1024 + kb, 128, 1024);
-          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, s ? 1u : 0u);
-          tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+          for (int s = 0; s < 4; ++s) {  // lo products first
+            const uint32_t kb = (uint32_t)s * 256;
+            tc::mma_tf32_ts(d, a + 32 + 8 * s, tc::desc(sbt + kb, 128, 1024), id, s ? 1u : 0u);
+            tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbt + 8 * 1024 + kb, 128, 1024), id, 1u);
+          }
+#pragma unroll
+          for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbt + (uint32_t)s * 256, 128, 1024), id, 1u);
+          tc::commit(&dt_full[b]);
         }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbt + (uint32_t)s * 256, 128, 1024), id, 1u);
-        tc::commit(&dt_full[b]);
         tc::commit(&at_empty);
       }
     }
@@ -428,38 +435,64 @@ __global__ void __launch_bounds__(kThreads3, 1)
         for (int ky = 0; ky < g.ry; ++ky) tc::bulk_load(vdst + ky * blk, in + xk_row(g, bb, ch, xl, ky), blk, &v_full);
       }
     }
+  } else if (warp == wTw3) {
+    // ======================= Y' twiddles, one 16-y pass at a time =======================
+    // rows n = (out re | out im, y 16), K = (ky re | ky im): e^{+i ky y}
+    // value: out re: C on re, -S on im; out im: S on re, C on im
+    const int ky = lane & 15, y8 = 8 * (lane >> 4);
+    const bool ky_ok = ky < g.ry;
+    const int f = mode_freq(ky, Ny, g.my);
+    float* hi = reinterpret_cast<float*>(by);
+    float* lo = hi + kBYPlane3 / 4;
+    int pass_i = 0;
+    for (int si = 0; si < my_slabs; ++si) {
+      for (int p = 0; p < L.npass; ++p, ++pass_i) {
+        tc::mbar_wait_lazy(&by_empty, (pass_i & 1) ^ 1, 64);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int yl = y8 + j, y = 16 * p + yl;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ky_ok && y < Ny) v = ph[(f * y) % Ny];
+          const int o_rr = kmaj3(yl, ky) / 4, o_ri = kmaj3(yl, 16 + ky) / 4;
+          const int o_ir = kmaj3(16 + yl, ky) / 4, o_ii = kmaj3(16 + yl, 16 + ky) / 4;
+          hi[o_rr] = v.x; lo[o_rr] = v.y;
+          hi[o_ri] = -v.z; lo[o_ri] = -v.w;
+          hi[o_ir] = v.z; lo[o_ir] = v.w;
+          hi[o_ii] = v.x; lo[o_ii] = v.y;
+        }
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&by_full);
+      }
+    }
   } else {
-    // ======================= MMA Z' (TS, N = 64), tile parity =======================
+    // ======================= MMA Z' (TS, N = 64 per z block), tile parity =======================
     const int k = warp - wIssZ3;
     if (lane == 0) {
       const uint32_t id = tc::idesc_tf32(128, 64);
-      const uint32_t sbz = tc::smem_u32(bz);
+      const uint32_t sbz0 = tc::smem_u32(bz);
+      int v = 0;  // D_Z[k] fill count
       for (int zi = k; zi < n_ztiles; zi += 2) {
-        const int ph = (zi >> 1) & 1;
-        DFNO_W(0, tc::mbar_wait(&az_full[k], ph));
-        DFNO_W(1, tc::mbar_wait(&dz_empty[k], ph ^ 1));
+        tc::mbar_wait(&az_full[k], (zi >> 1) & 1);
         tc::fence_after();
         const uint32_t a = tmem + jAZ + 64 * k, d = tmem + jDZ + 64 * k;
+        for (int zo = 0; zo < L.nzo; ++zo, ++v) {
+          tc::mbar_wait(&dz_empty[k], (v & 1) ^ 1);
+          tc::fence_after();
+          const uint32_t sbz = sbz0 + zo * kBlk3;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {  // lo products first, hi.hi last (see the Y' issuer)
-          const uint32_t kb = (uint32_t)s * 256;
-          const uint64_t bh = tc::desc(sbz + kb, 128, 1024), bl = tc::desc(sbz + 8 * 1024 + kb, 128, 1024);
-          tc::mma_tf32_ts(d, a + 32 + 8 * s, bh, id, s ? 1u : 0u);
-          tc::mma_tf32_ts(d, a + 8 * s, bl, id, 1u);
+          for (int s = 0; s < 4; ++s) {  // lo products first
+            const uint32_t kb = (uint32_t)s * 256;
+            tc::mma_tf32_ts(d, a + 32 + 8 * s, tc::desc(sbz + kb, 128, 1024), id, s ? 1u : 0u);
+            tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbz + 8 * 1024 + kb, 128, 1024), id, 1u);
+          }
+#pragma unroll
+          for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbz + (uint32_t)s * 256, 128, 1024), id, 1u);
+          tc::commit(&dz_full[k]);
         }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) tc::mma_tf32_ts(d, a + 8 * s, tc::desc(sbz + (uint32_t)s * 256, 128, 1024), id, 1u);
-        tc::commit(&dz_full[k]);
         tc::commit(&az_empty[k]);
       }
     }
   }
-  if (prof && lane == 0) {
-    const long long tot = clock64() - t_start;
-    for (int i = 0; i < 4; ++i) atomicAdd(prof + warp * 5 + i, (unsigned long long)wt[i]);
-    atomicAdd(prof + warp * 5 + 4, (unsigned long long)tot);
-  }
-#undef DFNO_W
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -488,7 +521,7 @@ int smem_cap_3() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (n <= 0) n = 227 * 1024;
-    n -= 2048 + 1024;
+    n -= 1024 + 512;  // alignment slack, static shared memory (barriers)
   }
   return n;
 }
@@ -497,9 +530,8 @@ int smem_cap_3() {
 
 int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
   if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;
-  if (g.nz > 64 || g.nt > 32) return DFNO_ERR_UNSUPPORTED;
   if ((g.rz * g.rt) % 2 != 0 || ((uintptr_t)in & 15)) return DFNO_ERR_UNSUPPORTED;  // 16-byte bulk copies
-  const Lay3 L = make_lay3(g.ny);
+  const Lay3 L = make_lay3(g.ny, g.nz, g.nt);
   if (L.total > smem_cap_3()) return DFNO_ERR_UNSUPPORTED;
   const bool fast = g.nz == 64 && g.nt == 32;
   auto kern = fast ? k_yzt_inv_tc3<true> : k_yzt_inv_tc3<false>;
@@ -507,22 +539,8 @@ int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cud
     return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   const int grid = sm_count_3() < slabs ? sm_count_3() : slabs;
-  static unsigned long long* prof = nullptr;
-  static const bool want_prof = getenv("DFNO_WAIT_PROFILE") && getenv("DFNO_WAIT_PROFILE")[0] == '1';
-  if (want_prof && !prof) cudaMalloc(&prof, kWarps3 * 5 * sizeof(unsigned long long));
-  if (prof) cudaMemsetAsync(prof, 0, kWarps3 * 5 * sizeof(unsigned long long), st);
-  kern<<<grid, kThreads3, L.total + 1024, st>>>(g, (const float2*)in, (float*)out, (float)scale, prof);
+  kern<<<grid, kThreads3, L.total + 1024, st>>>(g, (const float2*)in, (float*)out, (float)scale);
   DFNO_CUDA_CHECK_LAUNCH();
-  if (prof) {  // debug: per-warp wait cycles averaged over CTAs
-    unsigned long long h[kWarps3 * 5];
-    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    fprintf(stderr, "yzt_inv_tc3: per-CTA avg cycles  [w0 w1 w2 w3 | total]\n");
-    for (int w = 0; w < kWarps3; ++w)
-      fprintf(stderr, "  warp %2d: %9.0f %9.0f %9.0f %9.0f | %9.0f\n", w, h[w * 5] / (double)grid,
-              h[w * 5 + 1] / (double)grid, h[w * 5 + 2] / (double)grid, h[w * 5 + 3] / (double)grid,
-              h[w * 5 + 4] / (double)grid);
-  }
   return DFNO_OK;
 }
 

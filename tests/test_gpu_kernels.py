@@ -38,7 +38,8 @@ def tol(dtype):
 
 
 SHAPES = [((4, 64, 64, 32), (8, 8, 8, 8)), ((3, 32, 32, 16), (8, 8, 8, 8)), ((2, 30, 20, 22), (4, 8, 8, 8)),
-          ((2, 16, 16, 8), (4, 4, 4, 3)), ((2, 118, 64, 86), (8, 8, 8, 8)), ((2, 20, 12, 36), (8, 4, 5, 8))]
+          ((2, 16, 16, 8), (4, 4, 4, 3)), ((2, 118, 64, 86), (8, 8, 8, 8)), ((2, 20, 12, 36), (8, 4, 5, 8)),
+          ((2, 13, 10, 15), (4, 4, 4, 7)), ((1, 128, 128, 32), (8, 8, 8, 8)), ((1, 118, 64, 86), (8, 8, 6, 8))]
 
 
 @pytest.mark.parametrize("grid,modes", SHAPES)

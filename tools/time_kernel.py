@@ -74,4 +74,6 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20)
+    # TK_GRID=x,y,z,t selects another slab geometry (e.g. 33,118,64,86: one C4 P = 8 rank)
+    grid = tuple(int(v) for v in os.environ["TK_GRID"].split(",")) if os.environ.get("TK_GRID") else (64, 64, 64, 32)
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20, grid=grid)
