@@ -13,13 +13,9 @@ template <typename R>
 int xspec_fwd_simt(const dfno_geom&, const void*, const void*, void*, void*, cudaStream_t);
 template <typename R>
 int xspec_bwd_simt(const dfno_geom&, const void*, const void*, const void*, void*, void*, cudaStream_t);
-// tcgen05 tensor-core path (dft_yzt_tc.cu); returns DFNO_ERR_UNSUPPORTED
-// when the geometry is outside its envelope.
-int yzt_fwd_tc(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
-int yzt_inv_tc(const dfno_geom&, const void*, double, void*, cudaStream_t);
-// TMEM-operand tcgen05 path (dft_fwd_tc.cu)
+// tcgen05 paths (dft_fwd_tc.cu, dft_inv_tc3.cu); DFNO_ERR_UNSUPPORTED outside
+// their envelope (r > 16 or shared memory), which the SIMT kernels cover
 int yzt_fwd_tc2(const dfno_geom&, const void*, const void*, int, double, void*, cudaStream_t);
-int yzt_inv_tc2(const dfno_geom&, const void*, double, void*, cudaStream_t);
 int yzt_inv_tc3(const dfno_geom&, const void*, double, void*, cudaStream_t);
 // streamed x-spectral stage (xspec_stream.cu)
 size_t xspec_stream_workspace(const dfno_geom&);
@@ -43,21 +39,6 @@ bool check_blocks(const int32_t* starts, int extent, int P) {
     cur += base + (r < rem ? 1 : 0);
   }
   return starts[P] == extent;
-}
-
-bool env_flag(const char* name) {
-  const char* e = getenv(name);
-  return e && e[0] == '1';
-}
-
-// Environment switch for A/B measurements: DFNO_DISABLE_TC=1 forces SIMT.
-bool tc_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DFNO_DISABLE_TC");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
 }
 
 }  // namespace
@@ -127,15 +108,8 @@ extern "C" int dfno_dft_yzt_fwd(const dfno_geom* g, const void* src, const void*
   if (g->batch == 0) return DFNO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) {
-    if (tc_enabled()) {
-      static const bool v1 = env_flag("DFNO_YZT_V1");  // A/B switch: previous SMEM-operand kernel
-      if (!v1) {
-        rc = yzt_fwd_tc2(*g, src, pre, src_mode, scale, xk_out, st);
-        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-      }
-      rc = yzt_fwd_tc(*g, src, pre, src_mode, scale, xk_out, st);
-      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-    }
+    rc = yzt_fwd_tc2(*g, src, pre, src_mode, scale, xk_out, st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     return yzt_fwd_simt<float>(*g, src, pre, src_mode, scale, xk_out, st);
   }
   return yzt_fwd_simt<double>(*g, src, pre, src_mode, scale, xk_out, st);
@@ -148,20 +122,8 @@ extern "C" int dfno_dft_yzt_inv(const dfno_geom* g, const void* xk_in, double sc
   if (g->batch == 0) return DFNO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) {
-    if (tc_enabled()) {
-      static const bool v1 = env_flag("DFNO_YZT_V1");
-      static const bool inv2 = env_flag("DFNO_INV_V2");
-      if (!v1 && !inv2) {
-        rc = yzt_inv_tc3(*g, xk_in, scale, out, st);
-        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-      }
-      if (!v1) {
-        rc = yzt_inv_tc2(*g, xk_in, scale, out, st);
-        if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-      }
-      rc = yzt_inv_tc(*g, xk_in, scale, out, st);
-      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-    }
+    rc = yzt_inv_tc3(*g, xk_in, scale, out, st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     return yzt_inv_simt<float>(*g, xk_in, scale, out, st);
   }
   return yzt_inv_simt<double>(*g, xk_in, scale, out, st);

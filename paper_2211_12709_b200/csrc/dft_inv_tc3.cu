@@ -12,8 +12,8 @@
 //   loader   warp 20: V (16 contiguous (kz, kt) blocks per slab) -> shared, bulk
 //            copies one slab ahead
 //   twiddle  warp 21: the Y' operand of each 16-y pass (hi / lo planes) from a
-//            phase table into a one-slot buffer, so no N_y-sized table is
-//            resident
+//            phase table into a two-slot ring (one slot when shared memory is
+//            short), so no N_y-sized table is resident
 //   front    warps 0-3: V -> A_Y (shared), rows (kz, kt) [2 tiles], K = (ky re | ky im)
 //   MMA Y'   D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (SS, N=32,
 //            16 y per pass)
@@ -58,19 +58,20 @@ constexpr int kS2 = 65;                       // stash2 row pitch (floats)
 constexpr uint32_t jDY = 0, jAT = 64, jDT = 128, jAZ = 256, jDZ = 384;
 
 struct Lay3 {
-  int npass, nyc, ntb, nzo;
+  int npass, nyc, ntb, nzo, nby;
   int off_ay, off_by, off_bt, off_bz, off_ph, off_s1, off_s2, off_v, total;
 };
 
-__host__ __device__ inline Lay3 make_lay3(int ny, int nz, int nt) {
+__host__ __device__ inline Lay3 make_lay3(int ny, int nz, int nt, int nby) {
   Lay3 L;
+  L.nby = nby;
   L.npass = (ny + 15) / 16;
   L.nyc = (ny + 7) / 8;
   L.ntb = (nt + 31) / 32;
   L.nzo = (nz + 63) / 64;
   int o = 0;
   L.off_ay = o; o += 4 * kAYPlane3;      // tile 0 hi, tile 0 lo, tile 1 hi, tile 1 lo
-  L.off_by = o; o += 2 * kBYPlane3;      // one pass, hi | lo
+  L.off_by = o; o += nby * 2 * kBYPlane3;  // nby passes, hi | lo each
   L.off_bt = o; o += L.ntb * kBlk3;      // per t block: rows t re 32 | t im 32, hi | lo
   L.off_bz = o; o += L.nzo * kBlk3;      // per z block: rows z 64, hi | lo
   L.off_ph = o; o += ((16 * ny + 1023) / 1024) * 1024;  // e^{2 pi i j / N_y}: cos hi, cos lo, sin hi, sin lo
@@ -108,16 +109,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
 
 template <bool FAST>  // FAST: N_z == 64 and N_t == 32 (compile-time store offsets)
 __global__ void __launch_bounds__(kThreads3, 1)
-    k_yzt_inv_tc3(const dfno_geom g, const float2* __restrict__ in, float* __restrict__ out, float scale) {
+    k_yzt_inv_tc3(const dfno_geom g, const float2* __restrict__ in, float* __restrict__ out, float scale, int nby) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t v_full, v_empty, ay_full, ay_empty, dy_full, dy_empty, at_full, at_empty, by_full, by_empty;
+  __shared__ uint64_t v_full, v_empty, ay_full, ay_empty, dy_full, dy_empty, at_full, at_empty, by_full[2], by_empty[2];
   __shared__ uint64_t dt_full[2], dt_empty[2], az_full[2], az_empty[2], dz_full[2], dz_empty[2];
   __shared__ uint32_t tmem_base;
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
-  const Lay3 L = make_lay3(Ny, Nz, Nt);
+  const Lay3 L = make_lay3(Ny, Nz, Nt, nby);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* ay = smem + L.off_ay;
   unsigned char* by = smem + L.off_by;
@@ -158,8 +159,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
     tc::mbar_init(&dy_empty, 128);
     tc::mbar_init(&at_full, 128);
     tc::mbar_init(&at_empty, 1);
-    tc::mbar_init(&by_full, 32);
-    tc::mbar_init(&by_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&by_full[b], 32);
+      tc::mbar_init(&by_empty[b], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&dt_full[b], 1);
       tc::mbar_init(&dt_empty[b], 128);
@@ -364,13 +367,15 @@ __global__ void __launch_bounds__(kThreads3, 1)
     // ======================= MMA Y' (SS, N = 32) =======================
     if (lane == 0) {
       const uint32_t id = tc::idesc_tf32(128, 32);
-      const uint32_t say = tc::smem_u32(ay), sby = tc::smem_u32(by);
+      const uint32_t say = tc::smem_u32(ay);
       int pass_i = 0;
       for (int si = 0; si < my_slabs; ++si) {
         tc::mbar_wait_lazy(&ay_full, si & 1, 64);
         for (int p = 0; p < L.npass; ++p, ++pass_i) {
+          const int bs = pass_i % L.nby;
+          const uint32_t sby = tc::smem_u32(by + bs * 2 * kBYPlane3);
           tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1);
-          tc::mbar_wait(&by_full, pass_i & 1);
+          tc::mbar_wait(&by_full[bs], (pass_i / L.nby) & 1);
           tc::fence_after();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
               tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + kb, 128, 1024), id, 1u);
             }
           }
-          tc::commit(&by_empty);
+          tc::commit(&by_empty[bs]);
           tc::commit(&dy_full);
         }
         tc::commit(&ay_empty);
@@ -442,12 +447,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const int ky = lane & 15, y8 = 8 * (lane >> 4);
     const bool ky_ok = ky < g.ry;
     const int f = mode_freq(ky, Ny, g.my);
-    float* hi = reinterpret_cast<float*>(by);
-    float* lo = hi + kBYPlane3 / 4;
     int pass_i = 0;
     for (int si = 0; si < my_slabs; ++si) {
       for (int p = 0; p < L.npass; ++p, ++pass_i) {
-        tc::mbar_wait_lazy(&by_empty, (pass_i & 1) ^ 1, 64);
+        const int bs = pass_i % L.nby;
+        float* hi = reinterpret_cast<float*>(by + bs * 2 * kBYPlane3);
+        float* lo = hi + kBYPlane3 / 4;
+        tc::mbar_wait_lazy(&by_empty[bs], ((pass_i / L.nby) & 1) ^ 1, 64);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int yl = y8 + j, y = 16 * p + yl;
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
           hi[o_ii] = v.x; lo[o_ii] = v.y;
         }
         tc::fence_proxy_async();
-        tc::mbar_arrive(&by_full);
+        tc::mbar_arrive(&by_full[bs]);
       }
     }
   } else {
@@ -531,7 +537,8 @@ int smem_cap_3() {
 int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
   if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;
   if ((g.rz * g.rt) % 2 != 0 || ((uintptr_t)in & 15)) return DFNO_ERR_UNSUPPORTED;  // 16-byte bulk copies
-  const Lay3 L = make_lay3(g.ny, g.nz, g.nt);
+  Lay3 L = make_lay3(g.ny, g.nz, g.nt, 2);
+  if (L.total > smem_cap_3()) L = make_lay3(g.ny, g.nz, g.nt, 1);
   if (L.total > smem_cap_3()) return DFNO_ERR_UNSUPPORTED;
   const bool fast = g.nz == 64 && g.nt == 32;
   auto kern = fast ? k_yzt_inv_tc3<true> : k_yzt_inv_tc3<false>;
@@ -539,7 +546,7 @@ int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cud
     return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
   const int grid = sm_count_3() < slabs ? sm_count_3() : slabs;
-  kern<<<grid, kThreads3, L.total + 1024, st>>>(g, (const float2*)in, (float*)out, (float)scale);
+  kern<<<grid, kThreads3, L.total + 1024, st>>>(g, (const float2*)in, (float*)out, (float)scale, L.nby);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }

@@ -1,6 +1,6 @@
 // Truncated DFT over (y, z, t) of one rank's x-slab and its inverse --
 // generic SIMT path (fp32 and fp64, any extents).  The fp32 production path
-// for the common shapes is the tcgen05 kernel in dft_yzt_tc.cu; this file is
+// for the common shapes is the tcgen05 kernel in dft_fwd_tc.cu / dft_inv_tc3.cu; this file is
 // the reference-precision (real64) path and the fallback envelope.
 //
 // Forward replaces  fft_dims(a,(y,z,t)) + truncate_modes   (reference

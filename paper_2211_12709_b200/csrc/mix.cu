@@ -438,15 +438,6 @@ int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, cons
 int mix_fwd_tc(long long npts, int nb, int cin, int cout, const void* src, int src_act, int act, const void* w,
                void* pre, void* post, cudaStream_t st);
 
-static bool mix_tc_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DFNO_DISABLE_TC");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 }  // namespace dfno
 
 using namespace dfno;
@@ -458,10 +449,8 @@ extern "C" int dfno_mix_fwd(const dfno_geom* g, int64_t npts, int cin, int cout,
   if (npts == 0 || g->batch == 0) return DFNO_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (g->dtype == DFNO_F32) {
-    if (mix_tc_enabled()) {
-      const int rc = mix_fwd_tc(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
-      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-    }
+    const int rc = mix_fwd_tc(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     return mix_fwd_dispatch<float>(npts, g->batch, cin, cout, src, src_act, g->act, w, pre, post, st);
   }
   if (g->dtype == DFNO_F64)
@@ -486,16 +475,14 @@ extern "C" int dfno_mix_bwd(const dfno_geom* g, int64_t npts, int cin, int cout,
   if (src_act < 0 || src_act > 2) return DFNO_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
   if (src_act == 2) {  // fused act'(src) on the input gradient: tcgen05 path only
-    if (g->dtype != DFNO_F32 || !mix_tc_enabled() || !gin) return DFNO_ERR_UNSUPPORTED;
+    if (g->dtype != DFNO_F32 || !gin) return DFNO_ERR_UNSUPPORTED;
     return mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
                       mix_bwd_blocks(npts, g->batch), st);
   }
   if (g->dtype == DFNO_F32) {
-    if (mix_tc_enabled()) {
-      const int rc = mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
-                                mix_bwd_blocks(npts, g->batch), st);
-      if (rc != DFNO_ERR_UNSUPPORTED) return rc;
-    }
+    const int rc = mix_bwd_tc(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials,
+                              mix_bwd_blocks(npts, g->batch), st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
     return mix_bwd_dispatch<float>(npts, g->batch, cin, cout, gout, pre, src, src_act, g->act, w, gin, partials, st);
   }
   if (g->dtype == DFNO_F64)

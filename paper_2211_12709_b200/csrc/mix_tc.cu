@@ -642,12 +642,8 @@ static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const v
     if (sms <= 0) sms = 148;
   }
   const long long tiles = ((npts + kMbThreads - 1) / kMbThreads) * nb;
-  static const bool use_tma = [] {
-    const char* e = getenv("DFNO_MF_TMA");
-    return !(e && atoi(e) == 0);
-  }();
   CUtensorMap tm_src, tm_pre, tm_post;
-  if (use_tma && make_rows_map(&tm_src, src, npts, (long long)nb * cin, cin) &&
+  if (make_rows_map(&tm_src, src, npts, (long long)nb * cin, cin) &&
       make_rows_map(&tm_pre, pre, npts, (long long)nb * cout, cout) &&
       (!post || make_rows_map(&tm_post, post, npts, (long long)nb * cout, cout))) {
     if (!post) tm_post = tm_pre;
@@ -656,12 +652,7 @@ static int launch_mix_fwd_tc3(long long npts, int nb, int cin, int cout, const v
     // of >= 2 stages fits
     const int stage_bytes = cin * kMbThreads * 4, out_one = cout * kMbThreads * 4 * (post ? 2 : 1);
     const int static_bytes = 2 * 4096 + 256;
-    static const int max_per_sm = [] {
-      const char* e = getenv("DFNO_MF_CTAS");
-      const int v = e ? atoi(e) : 4;
-      return v < 1 ? 1 : (v > 4 ? 4 : v);
-    }();
-    int per_sm = max_per_sm, stages = 0, nbuf = 2;
+    int per_sm = 4, stages = 0, nbuf = 2;
     for (; per_sm >= 1; --per_sm) {  // double-buffered staging first, then single
       for (nbuf = 2; nbuf >= 1; --nbuf) {
         stages = ((227 * 1024) / per_sm - 1024 - static_bytes - nbuf * out_one) / stage_bytes;

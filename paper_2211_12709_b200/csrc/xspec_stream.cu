@@ -306,8 +306,6 @@ __global__ void __launch_bounds__(kXT, 3) k_xmix_bwd2(const dfno_geom g, const f
   }
 }
 
-int xdft_tc(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st);
-int xidft_tc(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st);
 
 namespace {
 int sms_x() {
@@ -322,14 +320,16 @@ int sms_x() {
 }
 
 // ---------------------------------------------------------------------------
-// Register-blocked x-DFTs (SIMT, N_x <= 128, r_x <= 16).  Both are small
-// complex GEMMs (16 x N_x by N_x x modes) that the FFMA issue rate bounds, so
-// each thread owns two modes (m, m + 32: coalesced across the warp) and eight
-// kx (forward) or all sixteen kx (inverse): every twiddle read from shared
-// memory (broadcast float4 = 2 twiddles) feeds 8 complex MACs, every data
-// load 8 or 16.  A block covers 256 modes of one (b, c).  Twiddles are fp32
-// sincospif (<= 1 ulp) with the exact integer phase reduction.
-constexpr int kXM = 256;
+// Register-blocked x-DFTs (SIMT, any N_x, r_x <= 16).  Both are small complex
+// GEMMs (16 x N_x by N_x x modes) that the FFMA issue rate bounds, so each
+// thread owns two modes (m, m + 32: coalesced across the warp) and eight kx
+// (forward) or all sixteen kx (inverse): every twiddle read from shared memory
+// (broadcast float4 = 2 twiddles) feeds 8 complex MACs, every data load 8 or
+// 16.  A block covers 256 / XS modes of one (b, c); when the modes per rank are
+// few (P = 8 ky pencils: 2 x 16 x 16) the x range is split XS ways across the
+// block's warps (forward: partial sums reduced through shared memory) so the
+// grid still fills the GPU.  Twiddles are fp32 sincospif (<= 1 ulp) with the
+// exact integer phase reduction.
 constexpr int kXB = 256;  // threads per block
 
 __device__ __forceinline__ void fill_tw16(float2* tw, long long* rows, const dfno_geom& g, int bb, int c) {
@@ -346,21 +346,26 @@ __device__ __forceinline__ void fill_tw16(float2* tw, long long* rows, const dfn
   for (int x = threadIdx.x; x < g.nx; x += blockDim.x) rows[x] = kx_row(g, bb, c, x);
 }
 
+// warps: kh = w & 1 (kx half), q = w >> 1 = (x part xs, mode group mg)
+template <int XS>
 __global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2* __restrict__ kx_in, float s1,
                                                 float2* __restrict__ X) {
+  constexpr int MG = 4 / XS, kM = 64 * MG;
   extern __shared__ __align__(16) unsigned char xs_raw[];
   const int Nx = g.nx;
   float2* tw = reinterpret_cast<float2*>(xs_raw);  // [Nx][16]
   long long* rows = reinterpret_cast<long long*>(tw + Nx * 16);
   const long long mloc = mloc_of(g);
-  const long long mtiles = (mloc + kXM - 1) / kXM;
-  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kXM;
+  const long long mtiles = (mloc + kM - 1) / kM;
+  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kM;
   const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
   fill_tw16(tw, rows, g, bb, c);
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, kh = w & 1;
-  const long long ma = m0 + (w >> 1) * 64 + lane, mb = ma + 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, kh = w & 1, q = w >> 1;
+  const int mg = q % MG, xs = q / MG;
+  const long long ma = m0 + mg * 64 + lane, mb = ma + 32;
   const bool oka = ma < mloc, okb = mb < mloc;
+  const int xlo = (int)((long long)Nx * xs / XS), xhi = (int)((long long)Nx * (xs + 1) / XS);
   float2 acc[2][8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[0][j] = acc[1][j] = make_float2(0.f, 0.f);
@@ -372,14 +377,14 @@ __global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2*
 #pragma unroll
     for (int u = 0; u < kPf; ++u) {
       const int x = x0 + u;
-      const float2* src = kx_in + rows[x < Nx ? x : 0];
-      za[u] = (oka && x < Nx) ? __ldcs(src + ma) : make_float2(0.f, 0.f);
-      zb[u] = (okb && x < Nx) ? __ldcs(src + mb) : make_float2(0.f, 0.f);
+      const float2* src = kx_in + rows[x < xhi ? x : xlo];
+      za[u] = (oka && x < xhi) ? __ldcs(src + ma) : make_float2(0.f, 0.f);
+      zb[u] = (okb && x < xhi) ? __ldcs(src + mb) : make_float2(0.f, 0.f);
     }
   };
-  fetch(0);
+  fetch(xlo);
 #pragma unroll 1
-  for (int x0 = 0; x0 < Nx; x0 += kPf) {
+  for (int x0 = xlo; x0 < xhi; x0 += kPf) {
     float2 ca[kPf], cb[kPf];
 #pragma unroll
     for (int u = 0; u < kPf; ++u) {
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2*
     fetch(x0 + kPf);
 #pragma unroll
     for (int u = 0; u < kPf; ++u) {
-      const int x = min(x0 + u, Nx - 1);  // x >= Nx carries zero data
+      const int x = min(x0 + u, xhi - 1);  // x >= xhi carries zero data
 #pragma unroll
       for (int j2 = 0; j2 < 4; ++j2) {
         const float4 t = t4[x * 8 + j2];
@@ -400,6 +405,31 @@ __global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2*
         cmac<float>(acc[1][2 * j2 + 1], cb[u], t1);
       }
     }
+  }
+  if constexpr (XS > 1) {
+    // partial sums of x parts 1.. -> shared (aliases the twiddles), x part 0 adds them in order
+    __syncthreads();
+    float2* red = tw;  // [xs - 1][kh][mg][j][half][lane]
+    if (xs > 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float2* r = red + ((((xs - 1) * 2 + kh) * MG + mg) * 8 + j) * 64 + lane;
+        r[0] = acc[0][j];
+        r[32] = acc[1][j];
+      }
+    }
+    __syncthreads();
+    if (xs > 0) return;
+#pragma unroll
+    for (int p = 1; p < XS; ++p)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2* r = red + ((((p - 1) * 2 + kh) * MG + mg) * 8 + j) * 64 + lane;
+        acc[0][j].x += r[0].x;
+        acc[0][j].y += r[0].y;
+        acc[1][j].x += r[32].x;
+        acc[1][j].y += r[32].y;
+      }
   }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -412,18 +442,21 @@ __global__ void __launch_bounds__(kXB) k_xdft_s(const dfno_geom g, const float2*
   }
 }
 
+// warps: xt = w % (2 XS) (x part), mg = w / (2 XS) (mode group)
+template <int XS>
 __global__ void __launch_bounds__(kXB) k_xidft_s(const dfno_geom g, const float2* __restrict__ Y, float s2,
                                                  float2* __restrict__ kx_out) {
+  constexpr int MG = 4 / XS, XT = 2 * XS, kM = 64 * MG;
   extern __shared__ __align__(16) unsigned char xs_raw[];
   const int Nx = g.nx;
   float2* tw = reinterpret_cast<float2*>(xs_raw);  // [Nx][16]
   long long* rows = reinterpret_cast<long long*>(tw + Nx * 16);
   const long long mloc = mloc_of(g);
-  const long long mtiles = (mloc + kXM - 1) / kXM;
-  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kXM;
+  const long long mtiles = (mloc + kM - 1) / kM;
+  const long long bc = blockIdx.x / mtiles, m0 = (blockIdx.x - bc * mtiles) * kM;
   const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xh = w & 1;
-  const long long ma = m0 + (w >> 1) * 64 + lane, mb = ma + 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, xt = w % XT, mg = w / XT;
+  const long long ma = m0 + mg * 64 + lane, mb = ma + 32;
   const bool oka = ma < mloc, okb = mb < mloc;
   float2 ya[16], yb[16];
 #pragma unroll
@@ -435,7 +468,7 @@ __global__ void __launch_bounds__(kXB) k_xidft_s(const dfno_geom g, const float2
   fill_tw16(tw, rows, g, bb, c);
   __syncthreads();
   const float4* t4 = reinterpret_cast<const float4*>(tw);
-  const int xa = xh ? (Nx + 1) / 2 : 0, xb = xh ? Nx : (Nx + 1) / 2;
+  const int xa = (int)((long long)Nx * xt / XT), xb = (int)((long long)Nx * (xt + 1) / XT);
 #pragma unroll 2
   for (int x = xa; x < xb; ++x) {
     float2 a = make_float2(0.f, 0.f), b = make_float2(0.f, 0.f);
@@ -454,15 +487,9 @@ __global__ void __launch_bounds__(kXB) k_xidft_s(const dfno_geom g, const float2
   }
 }
 
-int xdft_mode() {  // 0: tiled SIMT (default), 1: tcgen05, for A/B measurements (DFNO_XDFT=tc)
-  static const int v = [] {
-    const char* e = getenv("DFNO_XDFT");
-    return (e && e[0] == 't') ? 1 : 0;
-  }();
-  return v;
+bool tiled_ok(const dfno_geom& g) {
+  return g.dtype == DFNO_F32 && g.rx <= 16 && (size_t)g.nx * (16 * sizeof(float2) + sizeof(long long)) <= 200 * 1024;
 }
-
-bool tiled_ok(const dfno_geom& g) { return g.dtype == DFNO_F32 && g.rx <= 16 && g.nx <= 128; }
 
 unsigned grid_for(long long n, int per_sm = 8) {
   long long b = (n + kXT - 1) / kXT;
@@ -470,17 +497,36 @@ unsigned grid_for(long long n, int per_sm = 8) {
   return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+// x split: the smallest XS whose grid (b c ceil(modes / (256 / XS)) blocks)
+// covers two blocks per SM
+int x_split(const dfno_geom& g) {
+  const long long mloc = (long long)ky_local(g) * g.rz * g.rt, bc = (long long)g.batch * g.c;
+  for (int xs = 1; xs < 4; xs *= 2)
+    if (bc * ((mloc + 256 / xs - 1) / (256 / xs)) >= 2LL * sms_x()) return xs;
+  return 4;
+}
+
+template <typename K>
+int launch_tiled(K kern, const dfno_geom& g, int xs, const void* in, float s, void* out, cudaStream_t st) {
+  const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
+  const long long blocks = (long long)g.batch * g.c * ((mloc + 256 / xs - 1) / (256 / xs));
+  size_t smem = (size_t)g.nx * (16 * sizeof(float2) + sizeof(long long));
+  if (smem < 32 * 1024) smem = 32 * 1024;  // the forward's x-split reduction aliases the twiddles
+  if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return DFNO_ERR_UNSUPPORTED;
+  kern<<<(unsigned)blocks, kXB, smem, st>>>(g, (const float2*)in, s, (float2*)out);
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
 int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
-  if (tiled_ok(g) && xdft_mode() == 0) {
-    const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
-    const long long blocks = (long long)g.batch * g.c * ((mloc + kXM - 1) / kXM);
-    const size_t smem = (size_t)g.nx * 16 * sizeof(float2) + (size_t)g.nx * sizeof(long long);
-    k_xdft_s<<<(unsigned)blocks, kXB, smem, st>>>(g, (const float2*)kx_in, s1, (float2*)X);
-    DFNO_CUDA_CHECK_LAUNCH();
-    return DFNO_OK;
+  if (tiled_ok(g)) {
+    const int xs = x_split(g);
+    const int rc = xs == 1 ? launch_tiled(k_xdft_s<1>, g, 1, kx_in, s1, X, st)
+                   : xs == 2 ? launch_tiled(k_xdft_s<2>, g, 2, kx_in, s1, X, st)
+                             : launch_tiled(k_xdft_s<4>, g, 4, kx_in, s1, X, st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   }
-  const int rc = xdft_tc(g, kx_in, s1, X, st);  // tcgen05 path (N_x <= 128, r_x <= 16)
-  if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
   const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt * 2;
   auto k = g.rx <= 16 ? k_xdft<8, 2> : k_xdft<16, 2>;
@@ -492,16 +538,13 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
 }
 
 int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
-  if (tiled_ok(g) && xdft_mode() == 0) {
-    const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
-    const long long blocks = (long long)g.batch * g.c * ((mloc + kXM - 1) / kXM);
-    const size_t smem = (size_t)g.nx * 16 * sizeof(float2) + (size_t)g.nx * sizeof(long long);
-    k_xidft_s<<<(unsigned)blocks, kXB, smem, st>>>(g, (const float2*)Y, s2, (float2*)kx_out);
-    DFNO_CUDA_CHECK_LAUNCH();
-    return DFNO_OK;
+  if (tiled_ok(g)) {
+    const int xs = x_split(g);
+    const int rc = xs == 1 ? launch_tiled(k_xidft_s<1>, g, 1, Y, s2, kx_out, st)
+                   : xs == 2 ? launch_tiled(k_xidft_s<2>, g, 2, Y, s2, kx_out, st)
+                             : launch_tiled(k_xidft_s<4>, g, 4, Y, s2, kx_out, st);
+    if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   }
-  const int rc = xidft_tc(g, Y, s2, kx_out, st);
-  if (rc != DFNO_ERR_UNSUPPORTED) return rc;
   const size_t smem = (size_t)g.nx * g.rx * sizeof(float2);
   const long long n = (long long)g.batch * g.c * (long long)ky_local(g) * g.rz * g.rt;
   auto k = g.rx <= 16 ? k_xidft<16, 1> : k_xidft<32, 1>;
