@@ -120,9 +120,38 @@ class ThreadWorld:
         self.timeout = timeout
         self._barrier = threading.Barrier(world_size)
         self._slots = [None] * world_size
+        self._done = [None] * world_size
 
     def backend(self, rank: int) -> "ThreadBackend":
         return ThreadBackend(self, rank)
+
+
+def _stream_event(device):
+    """An event recorded on the calling thread's current CUDA stream (None
+    without CUDA): rank threads may run on different streams, so every
+    cross-rank read waits for the producer's event and every owner waits for
+    its readers' events before the buffer can be reused."""
+    if device.type != "cuda":
+        return None
+    ev = torch.cuda.Event()
+    ev.record()
+    return ev
+
+
+def _wait(ev) -> None:
+    if ev is not None:
+        torch.cuda.current_stream().wait_event(ev)
+
+
+def _private(obj):
+    """Copy every tensor in a posted payload onto the reader's stream."""
+    if isinstance(obj, torch.Tensor):
+        return obj.clone()
+    if isinstance(obj, tuple):
+        return tuple(_private(o) for o in obj)
+    if isinstance(obj, list):
+        return [_private(o) for o in obj]
+    return obj
 
 
 class ThreadBackend:
@@ -140,38 +169,54 @@ class ThreadBackend:
                 f"rank {self.rank} timed out at a collective; a peer likely skipped it"
             ) from None
 
-    def post_and_collect(self, tag: int, payload) -> list:
+    def _check_tags(self, tag, posted):
+        for peer, entry in enumerate(posted):
+            if entry[0] != tag:
+                return CollectiveMismatchError(
+                    f"rank {self.rank} issued {describe_tag(tag)} but rank {peer} issued {describe_tag(entry[0])}"
+                )
+        return None
+
+    def post_and_collect(self, tag: int, payload, collect: bool = True) -> list:
         """Publish (tag, payload); return every rank's payload in rank order
-        once all have arrived.  Tags must agree (reference comm.py:137-152)."""
-        self.world._slots[self.rank] = (tag, payload)
+        once all have arrived.  Tags must agree (reference comm.py:137-152).
+        Peers' tensors come back as private copies made on this rank's stream
+        after the producers' events, so no rank reads a buffer its owner may
+        still be writing or may free afterwards.  With ``collect=False`` this
+        rank only posts (peers' entries come back as None)."""
+        self.world._slots[self.rank] = (tag, payload, _stream_event(self.device))
         self._sync()
         posted = list(self.world._slots)
+        err = self._check_tags(tag, posted)
+        out = []
+        if err is None:
+            for peer, (_, p, ev) in enumerate(posted):
+                if peer == self.rank or not collect:
+                    out.append(p if peer == self.rank else None)
+                    continue
+                _wait(ev)
+                out.append(_private(p))
+        self.world._done[self.rank] = _stream_event(self.device)
         self._sync()  # nobody overwrites a slot before everyone has read it
-        for peer, (ptag, _) in enumerate(posted):
-            if ptag != tag:
-                raise CollectiveMismatchError(
-                    f"rank {self.rank} issued {describe_tag(tag)} but rank {peer} issued {describe_tag(ptag)}"
-                )
-        return [p for _, p in posted]
+        for peer, ev in enumerate(self.world._done):
+            if peer != self.rank:
+                _wait(ev)
+        if err is not None:
+            raise err
+        return out
 
     def exchange(self, tag, send, recv, send_counts, recv_counts):
-        # Device-to-device copies on the (shared) current stream: every rank's
-        # producer kernels were enqueued before the first barrier, every
-        # consumer is enqueued after the second.
-        self.world._slots[self.rank] = (tag, (send, list(send_counts)))
+        # Device-to-device copies on this rank's current stream, ordered after
+        # every producer's event; the owner waits for all readers' events
+        # before it may overwrite its send buffer.
+        self.world._slots[self.rank] = (tag, (send, list(send_counts)), _stream_event(self.device))
         self._sync()
         posted = list(self.world._slots)
-        err = None
-        for peer, (ptag, _) in enumerate(posted):
-            if ptag != tag:
-                err = CollectiveMismatchError(
-                    f"rank {self.rank} issued {describe_tag(tag)} but rank {peer} issued {describe_tag(ptag)}"
-                )
-                break
+        err = self._check_tags(tag, posted)
         if err is None:
             roff = 0
             for peer in range(self.world_size):
-                psend, pcounts = posted[peer][1]
+                _, (psend, pcounts), ev = posted[peer]
                 n = recv_counts[peer]
                 if n != pcounts[self.rank]:
                     err = CollectiveMismatchError(
@@ -180,9 +225,14 @@ class ThreadBackend:
                     break
                 soff = sum(pcounts[: self.rank])
                 if n:
+                    _wait(ev)
                     recv[roff : roff + n].copy_(psend[soff : soff + n])
                 roff += n
+        self.world._done[self.rank] = _stream_event(self.device)
         self._sync()
+        for peer, ev in enumerate(self.world._done):
+            if peer != self.rank:
+                _wait(ev)
         if err is not None:
             raise err
 
@@ -273,6 +323,7 @@ class Communicator:
         self.timeout = timeout
         self.stats = CommStats(rank=self.rank)
         self._seq = 0
+        self._bcast_meta = {}
 
     @classmethod
     def from_process_group(cls, group=None, device=None) -> "Communicator":
@@ -294,10 +345,11 @@ class Communicator:
         self._be.close()
 
     # ---- helpers -------------------------------------------------------
-    def _gather_all(self, tag: int, t: torch.Tensor) -> list:
-        """Every rank's tensor, in rank order (same shape on all ranks)."""
+    def _gather_all(self, tag: int, t: torch.Tensor, collect: bool = True) -> list:
+        """Every rank's tensor, in rank order (same shape on all ranks); with
+        ``collect=False`` on the thread backend this rank only contributes."""
         if self.threaded:
-            return self._be.post_and_collect(tag, t)
+            return self._be.post_and_collect(tag, t, collect)
         return self._be.all_gather_tensor(t)
 
     # ---- collectives ---------------------------------------------------
@@ -311,13 +363,29 @@ class Communicator:
             return t
         if self.threaded:
             payload = (t.labels, t.data) if self.rank == root else None
-            posted = self._be.post_and_collect(tag, payload)
+            posted = self._be.post_and_collect(tag, payload, collect=self.rank != root)
             labels, data = posted[root]
-            received = DenseTensor(labels, data.to(self.device).clone())
+            received = DenseTensor(labels, data.to(self.device))
         else:
-            labels, shape, dtype = self._be.broadcast_header(t, root)
-            buf = t.data.to(self.device).contiguous().clone() if t is not None else torch.empty(
-                shape, dtype=dtype.torch_dtype, device=self.device)
+            # The (labels, shape, dtype) header is read back once per label;
+            # later broadcasts under the same label reuse it, so the steady
+            # state has no device -> host synchronisation.  Every rank checks
+            # its own tensor against the header before any payload moves.
+            meta = self._bcast_meta.get(label) if label else None
+            if meta is None:
+                meta = self._be.broadcast_header(t, root)
+                if label:
+                    self._bcast_meta[label] = meta
+            labels, shape, dtype = meta
+            if t is not None and (tuple(t.labels) != tuple(labels) or tuple(t.shape) != tuple(shape)
+                                  or t.dtype != dtype):
+                raise CollectiveMismatchError(
+                    f"rank {self.rank} broadcast {label!r}: local {t.dims} {t.dtype} disagrees with the "
+                    f"root's {tuple(zip(labels, shape))} {dtype}")
+            if self.rank == root:
+                buf = t.data.to(self.device).contiguous()
+            else:
+                buf = torch.empty(shape, dtype=dtype.torch_dtype, device=self.device)
             self._be.broadcast_(buf, root)
             received = DenseTensor(labels, buf)
         if self.rank == root:
@@ -338,7 +406,7 @@ class Communicator:
         if self.world_size == 1:
             self.stats.record(REDUCE_SUM, 0, 0)
             return DenseTensor(t.labels, t.data.clone())
-        parts = self._gather_all(tag, t.data.to(self.device))
+        parts = self._gather_all(tag, t.data.to(self.device), collect=self.rank == root)
         if self.rank != root:
             self.stats.record(REDUCE_SUM, t.size, t.size * t.dtype.itemsize)
             return None
@@ -373,6 +441,39 @@ class Communicator:
         sent = n * (self.world_size - 1) if self.rank == 0 else 0
         self.stats.record(BROADCAST, sent, sent * item)
         return acc
+
+    def allreduce_sum_many(self, tensors: Sequence[torch.Tensor], labels: Sequence[str]) -> list:
+        """``reduce_sum`` to rank 0 then ``broadcast`` of several tensors in ONE
+        collective: the flattened tensors travel as one all-gather and every
+        rank sums the parts in rank order, so replicas are bit-identical with
+        no host synchronisation (reference fno_backward d/fno.py:501-508).
+        CommStats and tags are recorded exactly as the reference's sequence
+        reduce_sum(t0), reduce_sum(t1), ..., broadcast(t0), broadcast(t1), ..."""
+        P = self.world_size
+        for t, label in zip(tensors, labels):
+            self._next_tag(REDUCE_SUM, label)
+            n, item = t.numel(), t.element_size()
+            self.stats.record(REDUCE_SUM, 0 if self.rank == 0 or P == 1 else n, 0 if self.rank == 0 or P == 1 else n * item)
+        if P == 1:
+            out = list(tensors)
+        else:
+            sizes = [t.numel() for t in tensors]
+            flat = torch.cat([t.reshape(-1) for t in tensors])
+            tag = (zlib.crc32("|".join(labels).encode()) << 32) | (_PRIM_CODE[REDUCE_SUM] << 24) | (self._seq & 0xFFFFFF)
+            parts = self._gather_all(tag, flat)
+            acc = parts[0].clone()
+            for p in parts[1:]:
+                acc += p
+            out, off = [], 0
+            for t, n in zip(tensors, sizes):
+                out.append(acc[off : off + n].view(t.shape))
+                off += n
+        for t, label in zip(tensors, labels):
+            self._next_tag(BROADCAST, label + ".re")
+            n, item = t.numel(), t.element_size()
+            sent = n * (P - 1) if self.rank == 0 else 0
+            self.stats.record(BROADCAST, sent, sent * item)
+        return out
 
     def exchange(self, send: torch.Tensor, recv: torch.Tensor, send_counts: Sequence[int],
                  recv_counts: Sequence[int], label: str = "") -> None:
@@ -440,7 +541,7 @@ class Communicator:
             return DenseTensor(t.labels, data.clone())
         shape = list(t.shape)
         if self.threaded:
-            blocks = self._be.post_and_collect(tag, (t.labels, data))
+            blocks = self._be.post_and_collect(tag, (t.labels, data), collect=self.rank == root)
             if self.rank != root:
                 self.stats.record(GATHER, t.size, t.size * t.dtype.itemsize)
                 return None

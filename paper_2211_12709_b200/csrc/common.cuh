@@ -141,6 +141,97 @@ __device__ __forceinline__ R act_deriv(int act, R h) {
   return (R)1;
 }
 
+// ---- packed fp32x2 (FFMA2 / FMUL2 / FADD2 on sm_100a) ---------------------
+// Two lanes of fp32 arithmetic per issued instruction: the streaming kernels
+// that apply GELU / GELU' and the 3xTF32 split per element are issue-bound,
+// so the converters work on element pairs.
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
+
+// phi_fast on a pair (same polynomial, same MUFU approximations, so the
+// results are bit-identical to two phi_fast calls up to FMA contraction of
+// the unpacked form, which uses the same fused operations).
+__device__ __forceinline__ float2 phi_fast2(float2 h, float2& e) {
+  const float2 x = f2mul(make_float2(fabsf(h.x), fabsf(h.y)), f2s(0.70710678118654752f));
+  const float2 d = f2fma(f2s(0.3275911f), x, f2s(1.0f));
+  const float2 t = make_float2(rcp_approx(d.x), rcp_approx(d.y));
+  float2 p = f2fma(f2s(0.5307027145f), t, f2s(-0.7265760135f));
+  p = f2fma(p, t, f2s(0.7107068705f));
+  p = f2fma(p, t, f2s(-0.142248368f));
+  p = f2fma(p, t, f2s(0.127414796f));
+  p = f2mul(p, t);
+  const float2 a = f2mul(h, f2mul(h, f2s(-0.72134752044448170f)));
+  e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
+  const float2 q = f2mul(p, e);
+  const float2 r = f2fma(q, f2s(-1.0f), f2s(0.5f));  // 0.5 - q, exact
+  return f2add(f2s(0.5f), make_float2(copysignf(r.x, h.x), copysignf(r.y, h.y)));
+}
+
+template <int ACT>
+__device__ __forceinline__ float2 act_apply2(float2 h) {
+  if constexpr (ACT == DFNO_ACT_GELU) {
+    float2 e;
+    return f2mul(h, phi_fast2(h, e));
+  } else if constexpr (ACT == DFNO_ACT_RELU) {
+    return make_float2(h.x > 0.f ? h.x : 0.f, h.y > 0.f ? h.y : 0.f);
+  } else {
+    return h;
+  }
+}
+
+template <int ACT>
+__device__ __forceinline__ float2 act_deriv2(float2 h) {
+  if constexpr (ACT == DFNO_ACT_GELU) {
+    float2 e;
+    const float2 c = phi_fast2(h, e);
+    return f2fma(f2mul(h, f2s(0.3989422804014327f)), e, c);
+  } else if constexpr (ACT == DFNO_ACT_RELU) {
+    return make_float2(h.x > 0.f ? 1.f : 0.f, h.y > 0.f ? 1.f : 0.f);
+  } else {
+    return f2s(1.f);
+  }
+}
+
+// act and act' of the same pair (one phi evaluation)
+template <int ACT>
+__device__ __forceinline__ void act_both2(float2 h, float2& a, float2& d) {
+  if constexpr (ACT == DFNO_ACT_GELU) {
+    float2 e;
+    const float2 c = phi_fast2(h, e);
+    a = f2mul(h, c);
+    d = f2fma(f2mul(h, f2s(0.3989422804014327f)), e, c);
+  } else {
+    a = act_apply2<ACT>(h);
+    d = act_deriv2<ACT>(h);
+  }
+}
+
 // Rank helpers on the geometry.
 __host__ __device__ __forceinline__ int x_local(const dfno_geom& g) {
   return g.x_starts[g.rank + 1] - g.x_starts[g.rank];

@@ -131,10 +131,11 @@ __device__ __forceinline__ void cs(int k, int n, int N, int m, int r, double& c,
   }
 }
 
+// source conversion of an element pair: act(v), g * act'(pre) or raw
 template <int MODE, int ACT>
-__device__ __forceinline__ float conv(float v, float p) {
-  if (MODE == DFNO_SRC_ACT) return act_apply<float>(ACT, v);
-  if (MODE == DFNO_SRC_GRAD) return v * act_deriv<float>(ACT, p);
+__device__ __forceinline__ float2 conv2(float2 v, float2 p) {
+  if constexpr (MODE == DFNO_SRC_ACT) return act_apply2<ACT>(v);
+  if constexpr (MODE == DFNO_SRC_GRAD) return f2mul(v, act_deriv2<ACT>(p));
   return v;
 }
 
@@ -328,10 +329,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
           const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
           float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
           if constexpr (GRAD) p = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
-          tc::split_hl(conv<MODE, ACT>(q.x, p.x), h[4 * c4], l[4 * c4]);
-          tc::split_hl(conv<MODE, ACT>(q.y, p.y), h[4 * c4 + 1], l[4 * c4 + 1]);
-          tc::split_hl(conv<MODE, ACT>(q.z, p.z), h[4 * c4 + 2], l[4 * c4 + 2]);
-          tc::split_hl(conv<MODE, ACT>(q.w, p.w), h[4 * c4 + 3], l[4 * c4 + 3]);
+          const float2 a = conv2<MODE, ACT>(make_float2(q.x, q.y), make_float2(p.x, p.y));
+          const float2 b = conv2<MODE, ACT>(make_float2(q.z, q.w), make_float2(p.z, p.w));
+          tc::split_hl2(a, h[4 * c4], h[4 * c4 + 1], l[4 * c4], l[4 * c4 + 1]);
+          tc::split_hl2(b, h[4 * c4 + 2], h[4 * c4 + 3], l[4 * c4 + 2], l[4 * c4 + 3]);
         }
         if (half == 0) tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
         tc::tmem_st16(tmem + cAT + 64 * b + 16 * half + quarter_off, h);
@@ -365,7 +366,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
         __syncwarp();
         float h[16], l[16];
 #pragma unroll
-        for (int z = 0; z < 16; ++z) tc::split_hl(scr[(yy * 16 + lo16) * 17 + z], h[z], l[z]);
+        for (int z = 0; z < 16; z += 2)
+          tc::split_hl2(make_float2(scr[(yy * 16 + lo16) * 17 + z], scr[(yy * 16 + lo16) * 17 + z + 1]), h[z],
+                        h[z + 1], l[z], l[z + 1]);
         tc::tmem_st16(tmem + cAZ + 64 * b + 16 * part + quarter_off, h);
         tc::tmem_st16(tmem + cAZ + 64 * b + 32 + 16 * part + quarter_off, l);
         __syncwarp();

@@ -175,17 +175,30 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     const bool valid = p < npts;
     float gp[CM], a[CM];
     // gp = g * act'(pre) ; a = act(src) or src  (zero for padding / invalid points)
+    static_assert(CM % 2 == 0, "channel rows are converted in pairs");
 #pragma unroll
-    for (int o = 0; o < CM; ++o) gp[o] = gv[o] * act_deriv<float>(ACT, pv[o]);
+    for (int o = 0; o < CM; o += 2) {
+      const float2 v = f2mul(make_float2(gv[o], gv[o + 1]), act_deriv2<ACT>(make_float2(pv[o], pv[o + 1])));
+      gp[o] = v.x;
+      gp[o + 1] = v.y;
+    }
     if (gin_dact) {
 #pragma unroll
-      for (int i = 0; i < CM; ++i) {
-        a[i] = act_apply<float>(ACT, sv[i]);
-        dcur[i] = act_deriv<float>(ACT, sv[i]);
+      for (int i = 0; i < CM; i += 2) {
+        float2 av, dv;
+        act_both2<ACT>(make_float2(sv[i], sv[i + 1]), av, dv);
+        a[i] = av.x;
+        a[i + 1] = av.y;
+        dcur[i] = dv.x;
+        dcur[i + 1] = dv.y;
       }
     } else if (src_act) {
 #pragma unroll
-      for (int i = 0; i < CM; ++i) a[i] = act_apply<float>(ACT, sv[i]);
+      for (int i = 0; i < CM; i += 2) {
+        const float2 av = act_apply2<ACT>(make_float2(sv[i], sv[i + 1]));
+        a[i] = av.x;
+        a[i + 1] = av.y;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < CM; ++i) a[i] = sv[i];
@@ -206,9 +219,9 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
       // GEMM1 A operand (TMEM) and the GEMM2 B operand (shared memory)
       float h[32], l[32];
 #pragma unroll
-      for (int o = 0; o < 32; ++o) {
-        if (o < CM) tc::split_hl(gp[o], h[o], l[o]);
-        else h[o] = l[o] = 0.f;
+      for (int o = 0; o < 32; o += 2) {
+        if (o < CM) tc::split_hl2(make_float2(gp[o], gp[o + 1]), h[o], h[o + 1], l[o], l[o + 1]);
+        else h[o] = l[o] = h[o + 1] = l[o + 1] = 0.f;
       }
       if (want_gin) {
         tc::tmem_st32(a1h + lane_off, h);

@@ -13,6 +13,8 @@
 
 #include <stdint.h>
 
+#include "common.cuh"
+
 namespace dfno {
 namespace tc {
 
@@ -186,13 +188,19 @@ __device__ __forceinline__ uint32_t mbar_try_hint(uint64_t* bar, uint32_t parity
   return ok;
 }
 
-// Wait for the phase with the given parity to complete.  try_wait suspends
-// the thread for a hardware-bounded time instead of spinning.  Watchdog: ~2^28
-// failed polls (seconds) trap, turning a pipeline deadlock into a launch error
-// instead of a hung GPU.
+// Wait for the phase with the given parity to complete.  TRYWAIT parks the
+// warp in hardware until the barrier's phase flips (or a hardware time
+// limit), so the loop runs a handful of times per wait.  (The suspend-hint
+// form compiles to TRYWAIT + NANOSLEEP.SYNCS, which wakes on ANY barrier
+// traffic in the CTA: in the many-role pipelines its re-polls were ~30 % of
+// all issued instructions.)  Watchdog: ~2^28 failed polls trap, turning a
+// pipeline deadlock into a launch error instead of a hung GPU.
+#ifndef DFNO_WAIT_HINT
+#define DFNO_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
-  while (!mbar_try_hint(bar, parity)) {
+  while (!(DFNO_WAIT_HINT ? mbar_try_hint(bar, parity) : mbar_try(bar, parity))) {
     if (++n > (1u << 28)) __trap();
   }
 }
@@ -202,7 +210,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // warps doing work.
 __device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, uint32_t ns = 128) {
   uint32_t n = 0;
-  while (!mbar_try_hint(bar, parity)) {
+  while (!(DFNO_WAIT_HINT ? mbar_try_hint(bar, parity) : mbar_try(bar, parity))) {
     __nanosleep(ns);
     if (++n > (1u << 26)) __trap();
   }
@@ -313,6 +321,15 @@ __device__ __forceinline__ void split_rn(float x, float& hi, float& lo) {
 __device__ __forceinline__ void split_hl(float x, float& hi, float& lo) {
   hi = round_tf32(x);
   lo = x - hi;
+}
+
+// Pair form of split_hl: hi rounded per lane, lo = x - hi with one FFMA2.
+__device__ __forceinline__ void split_hl2(float2 x, float& h0, float& h1, float& l0, float& l1) {
+  h0 = round_tf32(x.x);
+  h1 = round_tf32(x.y);
+  const float2 l = f2fma(make_float2(h0, h1), f2s(-1.0f), x);
+  l0 = l.x;
+  l1 = l.y;
 }
 
 // ---- cp.async (LDGSTS): 16-, 8- and 4-byte copies with zero fill ---------

@@ -29,7 +29,6 @@ from __future__ import annotations
 import ctypes
 import enum
 import math
-import threading
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -461,8 +460,6 @@ class _Plan:
         return self.buf_a
 
 
-_PLANS: dict = {}
-_PLANS_LOCK = threading.Lock()
 _TIMER = None
 
 
@@ -484,22 +481,43 @@ def _launch(name: str, fn) -> None:
 
 
 def _plan(config: FnoConfig, comm: Communicator, batch: int) -> _Plan:
+    """The rank's plan (geometry, exchange buffers, xspec workspace), cached on
+    the Communicator itself so its device buffers are released together with
+    the rank's communicator (no process-wide cache that outlives rank threads)."""
     if not _lib.available():
         raise _lib.ExtensionMissingError("libdfno.so and a CUDA device are required (no CPU fallback)")
+    check_envelope(config)
     device = comm.device if comm.device.type == "cuda" else _default_device()
-    key = (config, comm.rank, comm.world_size, batch, str(device), threading.get_ident())
-    with _PLANS_LOCK:
-        plan = _PLANS.get(key)
-        if plan is None:
-            plan = _Plan(config, comm.rank, comm.world_size, batch, device)
-            _PLANS[key] = plan
+    key = (config, batch, str(device))
+    plans = comm.__dict__.setdefault("_dfno_plans", {})
+    plan = plans.get(key)
+    if plan is None:
+        plan = _Plan(config, comm.rank, comm.world_size, batch, device)
+        plans[key] = plan
     return plan
 
 
-def clear_plans() -> None:
-    """Drop cached plans and their scratch buffers."""
-    with _PLANS_LOCK:
-        _PLANS.clear()
+def clear_plans(comm: Optional[Communicator] = None) -> None:
+    """Drop the cached plans (and their scratch buffers) of ``comm``; plans
+    also go away with their communicator."""
+    if comm is not None:
+        comm.__dict__.pop("_dfno_plans", None)
+
+
+MAX_CHANNELS = 32  # mixer backward and fused x-spectral kernels hold a channel row in registers
+
+
+def check_envelope(config: FnoConfig) -> None:
+    """Reject, before any kernel runs, configurations outside the kernels'
+    envelope (the reference itself accepts any width): every channel count
+    must be <= MAX_CHANNELS."""
+    widths = {"in_channels": config.in_channels, "hidden_channels": config.hidden_channels,
+              "out_channels": config.out_channels}
+    wide = {k: v for k, v in widths.items() if v > MAX_CHANNELS}
+    if wide:
+        raise DimensionMismatchError(
+            f"channel widths {wide} exceed the B200 kernels' limit of {MAX_CHANNELS} channels "
+            f"(mixer backward and spectral contraction keep one channel row per thread)")
 
 
 def _on_device(t: DenseTensor, plan: _Plan, dtype: torch.dtype, what: str) -> torch.Tensor:
@@ -720,8 +738,7 @@ def fno_backward(comm: Communicator, g_local: DenseTensor, params: FnoParams, co
                              tag="enc")
 
     labels = (DimLabel.C, DimLabel.CO)
-    gwe = comm.reduce_sum(DenseTensor(labels, gwe_local), root=0, label="bwd.we")
-    gwd = comm.reduce_sum(DenseTensor(labels, gwd_local), root=0, label="bwd.wd")
-    gwe = comm.broadcast(gwe if comm.rank == 0 else DenseTensor(labels, gwe_local), root=0, label="bwd.we.re")
-    gwd = comm.broadcast(gwd if comm.rank == 0 else DenseTensor(labels, gwd_local), root=0, label="bwd.wd.re")
-    return _wrap(gx), FnoGrads(gwe, gwd, tuple(block_grads))
+    # reduce_sum + broadcast of both mixer gradients (d/fno.py:501-508) as one
+    # all-gather with a rank-ordered device sum: no host synchronisation
+    gwe_t, gwd_t = comm.allreduce_sum_many([gwe_local, gwd_local], ["bwd.we", "bwd.wd"])
+    return _wrap(gx), FnoGrads(DenseTensor(labels, gwe_t), DenseTensor(labels, gwd_t), tuple(block_grads))
