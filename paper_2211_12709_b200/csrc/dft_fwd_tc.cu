@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
+#ifdef DFNO_WAIT_PROF
+  const long long t_start = clock64();
+#endif
 
   const int slabs = g.batch * g.c * XL;
   const int my_slabs = (slabs - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
@@ -607,6 +610,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       }
     }
   }
+#ifdef DFNO_WAIT_PROF
+  tc::prof_life(t_start);
+#endif
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -678,6 +684,18 @@ int launch2_act(const dfno_geom& g, const void* src, const void* pre, double sca
 }
 
 }  // namespace
+
+#ifdef DFNO_WAIT_PROF
+// diagnostics build only: copy out (and clear) the per-(CTA, warp) wait /
+// lifetime cycle counters of the last yzt forward launches
+extern "C" int dfno_debug_wait_prof_fwd(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, tc::g_wait_prof, sizeof(tc::g_wait_prof));
+  static unsigned long long zero[tc::kProfCtas][tc::kProfWarps][2];
+  cudaMemcpyToSymbol(tc::g_wait_prof, zero, sizeof(zero));
+  return DFNO_OK;
+}
+#endif
 
 int yzt_fwd_tc2(const dfno_geom& g, const void* src, const void* pre, int mode, double scale, void* out,
                 cudaStream_t st) {

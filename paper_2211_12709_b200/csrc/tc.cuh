@@ -198,7 +198,38 @@ __device__ __forceinline__ uint32_t mbar_try_hint(uint64_t* bar, uint32_t parity
 #ifndef DFNO_WAIT_HINT
 #define DFNO_WAIT_HINT 0
 #endif
+// Diagnostics build only (tools/build_variant.py prof -DDFNO_WAIT_PROF): per
+// (CTA, warp) cycles spent inside mbarrier waits, plus each warp's lifetime,
+// read back with dfno_debug_wait_prof (abi.cu).  The shipped library has no
+// such state.
+#ifdef DFNO_WAIT_PROF
+constexpr int kProfCtas = 160, kProfWarps = 32;
+static __device__ unsigned long long g_wait_prof[kProfCtas][kProfWarps][2];
+struct WaitProf {
+  long long t0 = 0;
+  __device__ WaitProf() {
+#ifdef __CUDA_ARCH__
+    t0 = clock64();
+#endif
+  }
+  __device__ ~WaitProf() {
+#ifdef __CUDA_ARCH__
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < kProfCtas)
+      atomicAdd(&g_wait_prof[blockIdx.x][threadIdx.x >> 5][0], (unsigned long long)(clock64() - t0));
+#endif
+  }
+};
+__device__ __forceinline__ void prof_life(long long t_start) {
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < kProfCtas)
+    atomicAdd(&g_wait_prof[blockIdx.x][threadIdx.x >> 5][1], (unsigned long long)(clock64() - t_start));
+}
+#define DFNO_PROF_WAIT tc::WaitProf prof__
+#else
+#define DFNO_PROF_WAIT
+#endif
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  DFNO_PROF_WAIT;
   uint32_t n = 0;
   while (!(DFNO_WAIT_HINT ? mbar_try_hint(bar, parity) : mbar_try(bar, parity))) {
     if (++n > (1u << 28)) __trap();
@@ -209,6 +240,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // nanosleep between polls so the waiting warp leaves its issue slots to the
 // warps doing work.
 __device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, uint32_t ns = 128) {
+  DFNO_PROF_WAIT;
   uint32_t n = 0;
   while (!(DFNO_WAIT_HINT ? mbar_try_hint(bar, parity) : mbar_try(bar, parity))) {
     __nanosleep(ns);
@@ -218,6 +250,15 @@ __device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, u
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// One arrival per warp: the warp synchronises (which also orders each lane's
+// prior shared-memory and, after fence_before, tcgen05 operations) and one
+// lane arrives.  Barriers that count warps instead of threads see 32x fewer
+// arrive operations, and every arrive wakes the CTA's parked waiters.
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
