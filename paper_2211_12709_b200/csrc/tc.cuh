@@ -32,13 +32,15 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t 
   return d;
 }
 
-// Instruction descriptor: D fp32, A/B tf32, both K-major, M x N, optional
-// negation of A / B.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool neg_a = false, bool neg_b = false) {
+// Instruction descriptor: D fp32, A/B tf32, K-major unless a_mn / b_mn, M x N,
+// optional negation of A / B.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool neg_a = false, bool neg_b = false,
+                                                  bool a_mn = false, bool b_mn = false) {
   return (1u << 4)                      // c_format = F32
          | (2u << 7)                    // a_format = TF32
          | (2u << 10)                   // b_format = TF32
          | ((neg_a ? 1u : 0u) << 13) | ((neg_b ? 1u : 0u) << 14)
+         | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16)  // MN-major shared-memory operands
          | ((uint32_t)(N >> 3) << 17)   // n_dim
          | ((uint32_t)(M >> 4) << 24);  // m_dim
 }
