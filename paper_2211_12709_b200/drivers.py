@@ -46,7 +46,9 @@ from .fno import (
     predicted_block_volume,
     shard_params,
     slice_local,
+    _W_LABELS,
 )
+from .errors import ExtensionMissingError
 from .partition import Partition
 from .spectral import ModeSpec, retained_indices
 from .training import AdamState, global_output_count, train_step
@@ -245,26 +247,37 @@ def drive_comm_volume(comm: Communicator, opts: dict) -> Optional[dict]:
 def make_dataset(config: FnoConfig, samples: int, seed: int, device=None) -> tuple:
     """(inputs, targets) of the synthetic problem (reference d/bench.py:403-430):
     white-noise inputs pushed through a fixed random truncated-spectral
-    propagator.  The random draws are the reference's (numpy PCG64, same
-    order and shapes); the transforms and the per-mode channel mixing run in
-    float64 on ``device``; both tensors are returned there in the config's
-    real dtype, shaped (samples, c, Nx, Ny, Nz, Nt)."""
+    propagator.  The random draws are the reference's (numpy PCG64, same order
+    and shapes).  The propagator is itself one spectral block without
+    activation -- truncated x/y/z/t DFT, per-mode channel mixing, zero padding,
+    inverse DFT, real part -- so it runs on libdfno's block kernels
+    (``fno_block_forward``): with c = max(c_in, c_out) channels (zero-padded
+    inputs, the propagator embedded in a c x c weight W[i, o] = P[o, i]) and in
+    float64 like the reference, then cast once to the config's real dtype.
+    Both tensors are returned on ``device`` (a CUDA device: there is no host
+    path), shaped (samples, c, Nx, Ny, Nz, Nt)."""
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ExtensionMissingError("make_dataset runs its transforms on libdfno's CUDA kernels (no host path)")
     rng = np.random.default_rng(seed)
-    keep = [torch.from_numpy(retained_indices(n, m)).to(dev) for n, m in zip(config.grid, config.mode_counts)]
+    keep = [retained_indices(n, m) for n, m in zip(config.grid, config.mode_counts)]
     r_shape = tuple(len(k) for k in keep)
     cin, cout = config.in_channels, config.out_channels
     scale = 1.0 / np.sqrt(2.0 * cin)
     prop = scale * (rng.standard_normal((cout, cin) + r_shape) + 1j * rng.standard_normal((cout, cin) + r_shape))
     inputs = torch.from_numpy(rng.standard_normal((samples, cin) + config.grid)).to(dev)
-    spec = torch.fft.fftn(inputs, dim=(2, 3, 4, 5))
-    for d, k in enumerate(keep):
-        spec = spec.index_select(2 + d, k)
-    mixed = torch.einsum("bixyzt,oixyzt->boxyzt", spec, torch.from_numpy(prop).to(dev))
-    padded = torch.zeros((samples, cout) + config.grid, dtype=torch.complex128, device=dev)
-    kx, ky, kz, kt = keep
-    padded[:, :, kx[:, None, None, None], ky[None, :, None, None], kz[None, None, :, None], kt[None, None, None, :]] = mixed
-    targets = torch.fft.ifftn(padded, dim=(2, 3, 4, 5)).real
+    c = max(cin, cout)
+    block = FnoConfig(*config.grid, c, c, c, config.modes, 1, ActivationKind.IDENTITY, DType.REAL64, 1)
+    x = torch.zeros((samples, c) + config.grid, dtype=torch.float64, device=dev)
+    x[:, :cin] = inputs
+    w = torch.zeros((c, c) + r_shape, dtype=torch.complex128, device=dev)
+    w[:cin, :cout] = torch.from_numpy(np.ascontiguousarray(prop.transpose((1, 0) + tuple(range(2, 6))))).to(dev)
+
+    def body(comm):
+        return fno_block_forward(comm, DenseTensor(DATA_LABELS, x), DenseTensor(_W_LABELS, w), block,
+                                 label="dataset").data
+
+    targets = run_ranks(1, body, device=dev)[0][:, :cout]
     real = torch.float32 if config.dtype == DType.REAL32 else torch.float64
     return inputs.to(real).contiguous(), targets.to(real).contiguous()
 
