@@ -93,9 +93,13 @@ def _digest(t: torch.Tensor) -> str:
     return hashlib.sha256(t.detach().cpu().contiguous().numpy().tobytes()).hexdigest()
 
 
-def drive_parity_forward(comm: Communicator, opts: dict) -> Optional[dict]:
-    """Distributed forward vs the undistributed forward (reference
-    d/bench.py:100-124 with the P = 1 device forward as the reference)."""
+def drive_parity_forward(comm: Communicator, opts: dict, serial_forward=None) -> Optional[dict]:
+    """Distributed forward vs a serial forward on identical inputs and weights
+    (reference d/bench.py:100-124).  ``serial_forward(x_global, params,
+    serial_config) -> tensor`` is the reference's ``serial_fno_forward``
+    slot: the tests pass the all-at-once float64 oracle
+    (oracle/fno_oracle.py); without one the undistributed (P = 1) device
+    forward is the comparison."""
     config = config_from_opts(opts)
     batch, seed = opts.get("batch", 1), opts["seed"]
     dev = _device(comm)
@@ -110,8 +114,12 @@ def drive_parity_forward(comm: Communicator, opts: dict) -> Optional[dict]:
     if comm.rank != 0:
         return None
     serial_cfg = config_from_opts(dict(opts, workers=1))
-    ref = run_ranks(1, lambda c: fno_forward(c, x_global, params, serial_cfg), device=dev)[0]
-    return {"max_rel_err": _rel_err(gathered.data, ref.data),
+    if serial_forward is not None:
+        ref = serial_forward(x_global, params, serial_cfg)
+        ref = ref.data if isinstance(ref, DenseTensor) else ref
+    else:
+        ref = run_ranks(1, lambda c: fno_forward(c, x_global, params, serial_cfg), device=dev)[0].data
+    return {"max_rel_err": _rel_err(gathered.data, torch.as_tensor(ref, device=gathered.data.device)),
             "repart_calls_per_rank": delta.get(REPARTITION).calls,
             "repart_elements_total": int(elems), "output_digest": _digest(gathered.data)}
 

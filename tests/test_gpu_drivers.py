@@ -25,6 +25,26 @@ def test_comm_volume_equals_reference_run(golden_dir):
     assert got == want
 
 
+def _oracle_serial_forward(x_global, params, cfg):
+    """The reference's serial_fno_forward slot filled by the float64 numpy
+    oracle (all-at-once FFTs, oracle/fno_oracle.py)."""
+    from oracle import fno_oracle as O
+
+    blocks = [w.numpy().astype("complex128") for w in params.blocks]
+    return O.forward(x_global.numpy().astype("float64"), params.we.numpy().astype("float64"),
+                     params.wd.numpy().astype("float64"), blocks, cfg.mode_counts, cfg.activation.value)
+
+
+@pytest.mark.parametrize("dtype,tol", [("real64", 1e-10), ("real32", 1e-5)])
+def test_parity_against_serial_oracle(dtype, tol):
+    # SPEC criterion 1 as the reference runs it: distributed forward vs the
+    # serial all-at-once oracle (d/bench.py:100-124)
+    opts = {"grid": [16, 16, 16, 8], "modes": [4, 4, 4, 3], "channels": 2, "blocks": 4, "dtype": dtype, "seed": 7,
+            "workers": 8}
+    res = P.run_ranks(8, lambda comm: D.drive_parity_forward(comm, opts, serial_forward=_oracle_serial_forward))[0]
+    assert res["max_rel_err"] < tol
+
+
 @pytest.mark.parametrize("dtype,tol", [("real64", 1e-10), ("real32", 1e-5)])
 def test_parity_decomposition_invariance(dtype, tol):
     res = run(D.drive_parity_forward, {"grid": [16, 16, 16, 8], "modes": [4, 4, 4, 3], "channels": 2, "blocks": 4,

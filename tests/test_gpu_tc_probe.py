@@ -62,8 +62,26 @@ def test_tf32_mma_layouts(probe, case):
     assert err < 1e-5
 
 
-@pytest.fixture(scope="module")
-def perf():
+@pytest.mark.parametrize("M,N,K,lbo,sbo", [(128, 32, 32, 512, 2048), (128, 32, 32, 4096, 512), (128, 64, 8, 512, 2048)])
+def test_tf32_mma_mn_major_a(probe, M, N, K, lbo, sbo):
+    """MN-major tf32 A operand in the SWIZZLE_128B_BASE32B canonical form
+    (4 K rows x 128 B atoms, 32-byte chunks XOR k % 4; LBO = MN-atom stride,
+    SBO = 4-row K-group stride) -- the only MN-major tf32 layout the tensor
+    core accepts (tools/probe_mn.py: no-swizzle / plain 128B give zeros)."""
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    a, b = torch.tensor(A, device="cuda"), torch.tensor(B, device="cuda")
+    d = torch.zeros((M, N), device="cuda")
+    probe.probe_run_mn.restype = ctypes.c_int
+    rc = probe.probe_run_mn(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(d.data_ptr()),
+                            M, N, K, lbo, sbo, 128, (K // 4) * 128, 3)
+    assert rc == 0
+    want = trunc_tf32(A) @ trunc_tf32(B).T
+    assert np.max(np.abs(d.cpu().numpy() - want)) / np.max(np.abs(want)) < 1e-5
+
+
+def _perf_lib():
     src = ROOT / "tests" / "probes" / "probe_tc_perf.cu"
     so = ROOT / "tests" / "probes" / "libprobe_perf.so"
     if not so.exists() or so.stat().st_mtime < src.stat().st_mtime:
@@ -73,6 +91,11 @@ def perf():
     lib = ctypes.CDLL(str(so))
     lib.probe_perf_run.restype = ctypes.c_int
     return lib
+
+
+@pytest.fixture(scope="module")
+def perf():
+    return _perf_lib()
 
 
 def _perf(lib, mode, N, K, R, A=None, B=None):
@@ -100,7 +123,7 @@ def test_tf32_mma_a_from_tmem(perf):
         assert err < 1e-5, (N, K, err)
 
 
-def test_tcgen05_throughput_report(perf):
+def report_tcgen05_throughput(perf):
     """Cycle counts behind the DFT kernels' tiling choices (printed; -s)."""
     R = 256
     a = torch.randn(4096, 4096, device="cuda")
@@ -126,7 +149,7 @@ def test_tcgen05_throughput_report(perf):
     print(f"tcgen05.st 32x32b.x32 (4 warps, 16 KB): {st / R:.1f} cyc  -> {16384 * R / st:.0f} B/cyc")
 
 
-def test_tcgen05_issue_rate_report(perf):
+def report_tcgen05_issue_rate(perf):
     """Back-to-back MMA rate with precomputed descriptors (printed; -s)."""
     a = torch.randn(4096, 4096, device="cuda")
     for _ in range(50):
@@ -147,7 +170,7 @@ def test_tcgen05_issue_rate_report(perf):
                 print(f"{name} M=128 N={N:3d} P={Pn}: spinning lanes {out[0]:7.1f}  parked lanes {out[1]:7.1f} cyc/MMA")
 
 
-def test_tcgen05_lean_issue_report(perf):
+def report_tcgen05_lean_issue(perf):
     a = torch.randn(4096, 4096, device="cuda")
     for _ in range(50):
         a = a @ a
@@ -162,7 +185,7 @@ def test_tcgen05_lean_issue_report(perf):
         print(f"lean tf32 M=128 {n}: {int(cyc[0]) / (8 * 64):6.1f} cyc/MMA")
 
 
-def test_tcgen05_issue_under_contention_report(perf):
+def report_tcgen05_issue_under_contention(perf):
     a = torch.randn(4096, 4096, device="cuda")
     for _ in range(50):
         a = a @ a
@@ -174,3 +197,12 @@ def test_tcgen05_issue_under_contention_report(perf):
         for warps in (2, 8, 24):
             assert perf.probe_contention_run(R, bg, warps, ctypes.c_void_p(cyc.data_ptr())) == 0
             print(f"TS N=32 MMA issue, {warps - 1:2d} background warps ({name:10s}): {int(cyc[0]) / (8 * R):6.1f} cyc/MMA")
+
+
+# The microbenchmarks behind the kernels' tiling choices are reports, not
+# tests (they only print cycle counts):  python tests/test_gpu_tc_probe.py
+if __name__ == "__main__":
+    lib = _perf_lib()
+    for fn in (report_tcgen05_throughput, report_tcgen05_issue_rate, report_tcgen05_lean_issue,
+               report_tcgen05_issue_under_contention):
+        fn(lib)
