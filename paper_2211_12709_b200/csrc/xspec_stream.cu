@@ -26,6 +26,9 @@
 
 namespace dfno {
 
+int xdft_tc(const dfno_geom&, const void*, float, void*, cudaStream_t);
+int xidft_tc(const dfno_geom&, const void*, float, void*, cudaStream_t);
+
 namespace {
 constexpr int kXT = 256;  // threads per block
 constexpr int kOG = 4;    // output channels per thread in k_xmix / input channels in k_xmix_bwd
@@ -520,6 +523,8 @@ int launch_tiled(K kern, const dfno_geom& g, int xs, const void* in, float s, vo
 }
 
 int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
+  const int rt = xdft_tc(g, kx_in, s1, X, st);  // tcgen05 (xdft_tc.cu); SIMT outside its envelope
+  if (rt != DFNO_ERR_UNSUPPORTED) return rt;
   if (tiled_ok(g)) {
     const int xs = x_split(g);
     const int rc = xs == 1 ? launch_tiled(k_xdft_s<1>, g, 1, kx_in, s1, X, st)
@@ -538,6 +543,8 @@ int launch_dft(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStr
 }
 
 int launch_idft(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
+  const int rt = xidft_tc(g, Y, s2, kx_out, st);
+  if (rt != DFNO_ERR_UNSUPPORTED) return rt;
   if (tiled_ok(g)) {
     const int xs = x_split(g);
     const int rc = xs == 1 ? launch_tiled(k_xidft_s<1>, g, 1, Y, s2, kx_out, st)
