@@ -62,6 +62,7 @@ from .fno import (
 )
 from .partition import BlockRange, Partition, TransferBlock, block_decompose, range_intersection, repartition_plan
 from .dtns import gather_params, load_checkpoint, save_checkpoint, serialized_size, tensor_from_bytes, tensor_read, tensor_to_bytes, tensor_write
+from .graph import FwdBwdGraph
 from .staging import InputStager
 from .training import AdamState, adam_update, global_output_count, train_step
 from .spectral import ModeSpec, fft_dims, ifft_dims, pad_modes, retained_extent, retained_indices, truncate_modes
