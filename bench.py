@@ -90,7 +90,10 @@ def peaks():
 # ---------------------------------------------------------------------------
 
 
-def alg_bytes(cfg, xl, kyl, nranks):
+def alg_bytes(cfg, xl, kyl, nranks, groups=1):
+    """Compulsory HBM bytes per launch of each timed tag (DESIGN.md section 3);
+    with G channel groups (pipelined repartitions, N > 1) the yzt and x-DFT
+    launches each cover 1/G of the channels."""
     b, c, cin, cout = 1, cfg.hidden_channels, cfg.in_channels, cfg.out_channels
     ny, nz, nt = cfg.ny, cfg.nz, cfg.nt
     rx, ry, rz, rt = cfg.retained
@@ -101,16 +104,19 @@ def alg_bytes(cfg, xl, kyl, nranks):
     T_kx = 8 * b * c * cfg.nx * kyl * rz * rt
     S = 8 * b * c * rx * kyl * rz * rt
     W = 8 * c * c * rx * kyl * rz * rt
+    G = groups
     return {
         "mix_fwd.enc": Ain + A,
         "mix_fwd.dec": A + 2 * Aout,
-        "yzt_fwd.fwd": A + T_xk,
-        "yzt_fwd.bwd": 2 * A + T_xk,
-        "yzt_fwd.bwd_raw": A + T_xk,  # last block: act' fused into the decoder's mix_bwd
+        "yzt_fwd.fwd": (A + T_xk) / G,
+        "yzt_fwd.bwd": (2 * A + T_xk) / G,
+        "yzt_fwd.bwd_raw": (A + T_xk) / G,  # last block: act' fused into the decoder's mix_bwd
         "xspec_fwd": T_kx + W + S + T_kx,
         "xspec_bwd": T_kx + S + W + W + T_kx,
-        "yzt_inv.fwd": T_xk + A,
-        "yzt_inv.bwd": T_xk + A,
+        "xdft.fwd": (T_kx + S) / G, "xidft.fwd": (S + T_kx) / G, "xmix_fwd": 2 * S + W,
+        "xdft.bwd": (T_kx + S) / G, "xidft.bwd": (S + T_kx) / G, "xmix_bwd": 3 * S + 2 * W,
+        "yzt_inv.fwd": (T_xk + A) / G,
+        "yzt_inv.bwd": (T_xk + A) / G,
         "mix_bwd.dec": 2 * Aout + A + A,
         "mix_bwd.enc": 2 * A + Ain + Ain,
         "reduce.dec": 0,
@@ -422,7 +428,7 @@ def run_ours(args):
     if tf:
         tj = json.loads(tf[-1].read_text())
         traffic_tbl, traffic_src = tj.get("bytes_per_launch", {}), f"{tf[-1].name}: {tj.get('source', '')}"
-    ab = alg_bytes(cfg, xl, kyl, world)
+    ab = alg_bytes(cfg, xl, kyl, world, max(1, len(F._plan(cfg, comm, 1).groups)))
     dom = max(ksum.items(), key=lambda kv: kv[1][1])
     dname, (dn, dms) = dom
     davg = dms / dn
@@ -552,9 +558,10 @@ def run_single_gpu_config(args):
     # busiest rank's geometry (x_r = 33 / ky_r = 2 at C4, every rank at C3)
     xl = max(v[0] for v in times["xl"].values())
     kyl = max(v[1] for v in times["xl"].values())
-    ab = alg_bytes(cfg, xl, kyl, ranks)
+    G = min(F.PIPELINE_GROUPS, CHANNELS) if ranks > 1 else 1  # channel groups of the pipelined exchanges
+    ab = alg_bytes(cfg, xl, kyl, ranks, G)
     # mean per-launch bytes over ranks (uneven x slabs)
-    ab_mean = {k: sum(alg_bytes(cfg, v[0], v[1], ranks)[k] for v in times["xl"].values()) / ranks for k in ab}
+    ab_mean = {k: sum(alg_bytes(cfg, v[0], v[1], ranks, G)[k] for v in times["xl"].values()) / ranks for k in ab}
     kernels = {k: {"launches_per_step": n / args.steps, "avg_ms": round(t / n, 5),
                    "share": round(t / sum(v[1] for v in ksum.values()), 4),
                    "alg_GBps": round(ab_mean[k] / (t / n * 1e-3) / 1e9, 1) if ab_mean[k] else None,

@@ -192,6 +192,23 @@ int dfno_xspec_bwd_ws(const dfno_geom* g, const void* kx_in, const void* spec,
                       void* stream);
 
 /*
+ * The x-spectral stage by parts, fp32 (DFNO_ERR_UNSUPPORTED otherwise), so a
+ * caller can pipeline channel groups against the repartition exchanges: the
+ * x-DFTs of a group of channels run on a geometry whose c is the group size
+ * with X / Y offset to the group's first channel (b = 1), the contraction on
+ * the full geometry.  Same reference lines as dfno_xspec_fwd / _bwd.
+ *   dfno_xdft     X  = scale * fft_x(kx_in) truncated   (d/fno.py:331-332, :450-452)
+ *   dfno_xmix_fwd Y  = einsum_spectral(X, w)             (d/tensor.py:231-255)
+ *   dfno_xmix_bwd gw = sum_b conj(spec) D ; dX = sum_o D conj(w)  (d/fno.py:415-423)
+ *   dfno_xidft    kx_out = scale * sum_kx Y e^{+i}       (d/fno.py:335-336, :455-457)
+ */
+int dfno_xdft(const dfno_geom* g, const void* kx_in, double scale, void* X, void* stream);
+int dfno_xmix_fwd(const dfno_geom* g, const void* X, const void* w, void* Y, void* stream);
+int dfno_xmix_bwd(const dfno_geom* g, const void* spec, const void* D, const void* w, void* gw, void* dX,
+                  void* stream);
+int dfno_xidft(const dfno_geom* g, const void* Y, double scale, void* kx_out, void* stream);
+
+/*
  * Training step (reference train_step d/training.py:96-133): fused residual /
  * loss / output gradient, and Adam on the real view of a parameter.
  *   resid = pred - target; grad_out = grad_scale * resid (grad_out may be

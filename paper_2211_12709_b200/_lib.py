@@ -46,6 +46,7 @@ EXPORTS = (
     "dfno_mix_fwd", "dfno_mix_bwd_partials", "dfno_mix_bwd", "dfno_reduce_partials",
     "dfno_dft_yzt_fwd", "dfno_dft_yzt_inv", "dfno_xspec_fwd", "dfno_xspec_bwd",
     "dfno_xspec_workspace", "dfno_xspec_fwd_ws", "dfno_xspec_bwd_ws",
+    "dfno_xdft", "dfno_xmix_fwd", "dfno_xmix_bwd", "dfno_xidft",
     "dfno_mse_partials", "dfno_mse_grad", "dfno_adam",
 )
 
@@ -93,6 +94,10 @@ def load(path: Path = LIB_PATH) -> ctypes.CDLL:
         "dfno_xspec_workspace": ([gp, ctypes.POINTER(i64)], i32),
         "dfno_xspec_fwd_ws": ([gp, vp, vp, vp, vp, vp, vp], i32),
         "dfno_xspec_bwd_ws": ([gp, vp, vp, vp, vp, vp, vp, vp], i32),
+        "dfno_xdft": ([gp, vp, dbl, vp, vp], i32),
+        "dfno_xmix_fwd": ([gp, vp, vp, vp, vp], i32),
+        "dfno_xmix_bwd": ([gp, vp, vp, vp, vp, vp, vp], i32),
+        "dfno_xidft": ([gp, vp, dbl, vp, vp], i32),
         "dfno_mse_partials": ([i64, ctypes.POINTER(i32)], i32),
         "dfno_mse_grad": ([gp, i64, vp, vp, dbl, vp, vp, vp, vp], i32),
         "dfno_adam": ([gp, i64, vp, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp], i32),

@@ -476,11 +476,13 @@ class Communicator:
         return out
 
     def exchange(self, send: torch.Tensor, recv: torch.Tensor, send_counts: Sequence[int],
-                 recv_counts: Sequence[int], label: str = "") -> None:
+                 recv_counts: Sequence[int], label: str = "", record: bool = True) -> int:
         """Peer-major all-to-all(v) of packed buffers; counts in elements of
         ``send``'s dtype.  Recorded as one repartition with the off-rank
         element count, exactly as the reference's repartition
-        (comm.py:461-482)."""
+        (comm.py:461-482) -- unless ``record`` is false, for the chunks of a
+        pipelined repartition that ``record_repartition`` accounts once.
+        Returns the off-rank element count.  Runs on the current stream."""
         tag = self._next_tag(REPARTITION, label)
         if len(send_counts) != self.world_size or len(recv_counts) != self.world_size:
             raise ShapeMismatchError("one split size per rank is required")
@@ -491,7 +493,13 @@ class Communicator:
             self._be.exchange(tag, s, r, [k * n for n in send_counts], [k * n for n in recv_counts])
         elif send.data_ptr() != recv.data_ptr():
             recv.reshape(-1).copy_(send.reshape(-1))
-        self.stats.record(REPARTITION, off_rank, off_rank * send.element_size())
+        if record:
+            self.stats.record(REPARTITION, off_rank, off_rank * send.element_size())
+        return off_rank
+
+    def record_repartition(self, off_rank_elements: int, itemsize: int) -> None:
+        """Account one (chunked) repartition with its total off-rank elements."""
+        self.stats.record(REPARTITION, off_rank_elements, off_rank_elements * itemsize)
 
     def repartition(self, t: DenseTensor, src_part: Partition, dst_part: Partition, label: str = "") -> DenseTensor:
         """Move this rank's src slab to its dst slab (reference comm.py:421-483).

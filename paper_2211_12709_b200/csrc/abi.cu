@@ -21,6 +21,10 @@ int yzt_inv_tc3(const dfno_geom&, const void*, double, void*, cudaStream_t);
 size_t xspec_stream_workspace(const dfno_geom&);
 int xspec_fwd_stream(const dfno_geom&, const void*, const void*, void*, void*, void*, cudaStream_t);
 int xspec_bwd_stream(const dfno_geom&, const void*, const void*, const void*, void*, void*, void*, cudaStream_t);
+int xdft_stage(const dfno_geom&, const void*, float, void*, cudaStream_t);
+int xidft_stage(const dfno_geom&, const void*, float, void*, cudaStream_t);
+int xmix_fwd_stage(const dfno_geom&, const void*, const void*, void*, cudaStream_t);
+int xmix_bwd_stage(const dfno_geom&, const void*, const void*, const void*, void*, void*, cudaStream_t);
 }  // namespace dfno
 
 using namespace dfno;
@@ -179,4 +183,39 @@ extern "C" int dfno_xspec_bwd_ws(const dfno_geom* g, const void* kx_in, const vo
   const int r2 = xspec_bwd_stream(*g, kx_in, spec, w, gw, kx_out, work, (cudaStream_t)stream);
   if (r2 != DFNO_ERR_UNSUPPORTED) return r2;
   return dfno_xspec_bwd(g, kx_in, spec, w, gw, kx_out, stream);
+}
+
+// ---- the x-spectral stage by parts (fp32): lets the caller pipeline the
+// x-DFTs of channel groups against the exchanges (fno.py)
+extern "C" int dfno_xdft(const dfno_geom* g, const void* kx_in, double scale, void* X, void* stream) {
+  if (!g || !kx_in || !X) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  return xdft_stage(*g, kx_in, (float)scale, X, (cudaStream_t)stream);
+}
+
+extern "C" int dfno_xidft(const dfno_geom* g, const void* Y, double scale, void* kx_out, void* stream) {
+  if (!g || !Y || !kx_out) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  return xidft_stage(*g, Y, (float)scale, kx_out, (cudaStream_t)stream);
+}
+
+extern "C" int dfno_xmix_fwd(const dfno_geom* g, const void* X, const void* w, void* Y, void* stream) {
+  if (!g || !X || !w || !Y) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  return xmix_fwd_stage(*g, X, w, Y, (cudaStream_t)stream);
+}
+
+extern "C" int dfno_xmix_bwd(const dfno_geom* g, const void* spec, const void* D, const void* w, void* gw, void* dX,
+                             void* stream) {
+  if (!g || !spec || !D || !w || !gw || !dX) return DFNO_ERR_NULL;
+  const int rc = dfno_geom_validate(g);
+  if (rc != DFNO_OK) return rc;
+  if (g->batch == 0) return DFNO_OK;
+  return xmix_bwd_stage(*g, spec, D, w, gw, dX, (cudaStream_t)stream);
 }

@@ -572,14 +572,20 @@ size_t xspec_stream_workspace(const dfno_geom& g) {
   return 2 * (size_t)g.batch * g.c * g.rx * ky_local(g) * g.rz * g.rt * sizeof(float2);
 }
 
-int xspec_fwd_stream(const dfno_geom& g, const void* kx_in, const void* w, void* spec, void* kx_out, void* work,
-                     cudaStream_t st) {
+// the three stages on their own (channel-group pipelining in the Python
+// layer launches the x-DFTs per channel group around the exchanges)
+int xdft_stage(const dfno_geom& g, const void* kx_in, float s1, void* X, cudaStream_t st) {
   if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
-  const size_t half = xspec_stream_workspace(g) / 2;
-  void* X = spec ? spec : work;
-  void* Y = static_cast<char*>(work) + half;
-  int rc = launch_dft(g, kx_in, 1.f, X, st);  // fft_x unnormalised (d/spectral.py:36)
-  if (rc) return rc;
+  return launch_dft(g, kx_in, s1, X, st);
+}
+
+int xidft_stage(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
+  return launch_idft(g, Y, s2, kx_out, st);
+}
+
+int xmix_fwd_stage(const dfno_geom& g, const void* X, const void* w, void* Y, cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
   const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
   if (cols % 2 == 0)
     k_xmix2<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(g, (const float4*)X,
@@ -588,6 +594,35 @@ int xspec_fwd_stream(const dfno_geom& g, const void* kx_in, const void* w, void*
     k_xmix<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(g, (const float2*)X,
                                                                                 (const float2*)w, (float2*)Y);
   DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+int xmix_bwd_stage(const dfno_geom& g, const void* spec, const void* D, const void* w, void* gw, void* dX,
+                   cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
+  const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
+  if (cols % 2 == 0 && g.batch == 1) {
+    k_xmix_bwd2<1><<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(
+        g, (const float4*)spec, (const float4*)D, (const float4*)w, (float4*)gw, (float4*)dX);
+  } else {
+    auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
+    kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(
+        g, (const float2*)spec, (const float2*)D, (const float2*)w, (float2*)gw, (float2*)dX);
+  }
+  DFNO_CUDA_CHECK_LAUNCH();
+  return DFNO_OK;
+}
+
+int xspec_fwd_stream(const dfno_geom& g, const void* kx_in, const void* w, void* spec, void* kx_out, void* work,
+                     cudaStream_t st) {
+  if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
+  const size_t half = xspec_stream_workspace(g) / 2;
+  void* X = spec ? spec : work;
+  void* Y = static_cast<char*>(work) + half;
+  int rc = launch_dft(g, kx_in, 1.f, X, st);  // fft_x unnormalised (d/spectral.py:36)
+  if (rc) return rc;
+  rc = xmix_fwd_stage(g, X, w, Y, st);
+  if (rc) return rc;
   return launch_idft(g, Y, (float)(1.0 / g.nx), kx_out, st);  // ifft_x carries 1/Nx (d/spectral.py:49)
 }
 
@@ -599,16 +634,8 @@ int xspec_bwd_stream(const dfno_geom& g, const void* kx_in, const void* spec, co
   void* dX = static_cast<char*>(work) + half;
   int rc = launch_dft(g, kx_in, (float)(1.0 / g.nx), D, st);  // fft_x / Nx (d/fno.py:450-452)
   if (rc) return rc;
-  const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
-  if (cols % 2 == 0 && g.batch == 1) {
-    k_xmix_bwd2<1><<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(
-        g, (const float4*)spec, (const float4*)D, (const float4*)w, (float4*)gw, (float4*)dX);
-  } else {
-    auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
-    kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(
-        g, (const float2*)spec, (const float2*)D, (const float2*)w, (float2*)gw, (float2*)dX);
-  }
-  DFNO_CUDA_CHECK_LAUNCH();
+  rc = xmix_bwd_stage(g, spec, D, w, gw, dX, st);
+  if (rc) return rc;
   return launch_idft(g, dX, 1.f, kx_out, st);  // ifft_x * Nx = unnormalised inverse (d/fno.py:455-457)
 }
 

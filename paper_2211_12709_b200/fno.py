@@ -329,8 +329,32 @@ class FnoGrads:
 # ---------------------------------------------------------------------------
 
 
+# Channel groups of the pipelined repartitions.  Process-group worlds (NCCL
+# between GPUs) overlap each group's all-to-all with the next group's DFT;
+# thread worlds share one GPU, where the exchange is a device copy competing
+# for the same HBM and the split only costs wave quantisation, so they run
+# unsplit unless PIPELINE_GROUPS_THREADED asks for it (the tests do).
+PIPELINE_GROUPS = 2
+PIPELINE_GROUPS_THREADED = 1
+
+
+@dataclass
+class _Group:
+    c0: int
+    c1: int
+    geom: object
+    gp: object
+    xk_counts: list
+    kx_counts: list
+    a: torch.Tensor  # XK send (forward) / XK receive (return)
+    b: torch.Tensor  # KX receive
+    c: torch.Tensor  # KX send
+    spec_off: int    # first element of the group's channels in a (b = 1) spectrum
+
+
 class _Plan:
-    def __init__(self, config: FnoConfig, rank: int, world: int, batch: int, device: torch.device):
+    def __init__(self, config: FnoConfig, rank: int, world: int, batch: int, device: torch.device,
+                 threaded: bool = False):
         if world != config.num_ranks:
             raise ShapeMismatchError(f"config.num_ranks={config.num_ranks} but the communicator has {world} ranks")
         self.config = config
@@ -374,6 +398,39 @@ class _Plan:
         _lib.check(self.lib.dfno_xspec_workspace(self.gp, ctypes.byref(ws)), "xspec workspace")
         self.xspec_work = torch.empty(max(1, ws.value), dtype=torch.uint8, device=device)
         self.partials = {}
+        self.groups = self._channel_groups(xp, kp, rz, rt, PIPELINE_GROUPS_THREADED if threaded else PIPELINE_GROUPS)
+        self.comm_stream = torch.cuda.Stream(device=device) if self.groups else None
+
+    def _channel_groups(self, xp, kp, rz, rt, ngroups: int) -> list:
+        """Channel groups of the pipelined exchanges (world > 1, b = 1, fp32):
+        each group has its own geometry (c = group size) and its own
+        peer-major XK / KX regions carved from the plan's buffers, so group
+        k's all-to-all runs on the comm stream while group k + 1's DFT runs on
+        the compute stream."""
+        cfg, c = self.config, self.config.hidden_channels
+        ng = min(ngroups, c)
+        if self.world == 1 or self.batch != 1 or cfg.dtype != DType.REAL32 or ng < 2:
+            return []
+        bounds = [c * k // ng for k in range(ng + 1)]
+        groups, xo, ko = [], 0, 0
+        for k in range(ng):
+            c0, c1 = bounds[k], bounds[k + 1]
+            n = c1 - c0
+            geom = _lib.make_geom(
+                batch=1, c_in=n, c=n, c_out=n, grid=cfg.grid, modes=cfg.mode_counts, retained=cfg.retained,
+                nranks=self.world, rank=self.rank, dtype=_lib.F32, act=cfg.activation.code,
+                x_starts=xp.starts(), ky_starts=kp.starts())
+            _lib.check(self.lib.dfno_geom_validate(ctypes.byref(geom)), "group geometry")
+            xk = n * self.xl * cfg.retained_y * rz * rt
+            kx = n * cfg.nx * self.kyl * rz * rt
+            groups.append(_Group(
+                c0=c0, c1=c1, geom=geom, gp=ctypes.byref(geom),
+                xk_counts=[n * self.xl * kp.extent_of(p) * rz * rt for p in range(self.world)],
+                kx_counts=[n * xp.extent_of(p) * self.kyl * rz * rt for p in range(self.world)],
+                a=self.buf_a[xo:xo + xk], b=self.buf_b[ko:ko + kx], c=self.buf_c[ko:ko + kx],
+                spec_off=c0 * cfg.retained_x * self.kyl * rz * rt))
+            xo, ko = xo + xk, ko + kx
+        return groups
 
     # -- shapes ----------------------------------------------------------
     def act_shape(self, ch: int) -> tuple:
@@ -425,14 +482,61 @@ class _Plan:
             self.gp, nparts, cin * cout, _lib.ptr(buf), _lib.ptr(gw), _lib.stream_handle()), "dfno_reduce_partials"))
         return (gw, fused[0]) if fuse_src_dact else gw
 
-    def yzt_fwd(self, src, pre, mode, scale, out, tag="yzt_fwd"):
+    def yzt_fwd(self, src, pre, mode, scale, out, tag="yzt_fwd", gp=None):
         _launch(tag, lambda: _lib.check(self.lib.dfno_dft_yzt_fwd(
-            self.gp, _lib.ptr(src), _lib.ptr(pre), mode, float(scale), _lib.ptr(out), _lib.stream_handle()),
+            gp or self.gp, _lib.ptr(src), _lib.ptr(pre), mode, float(scale), _lib.ptr(out), _lib.stream_handle()),
             "dfno_dft_yzt_fwd"))
 
-    def yzt_inv(self, xk_in, scale, out, tag="yzt_inv"):
+    def yzt_inv(self, xk_in, scale, out, tag="yzt_inv", gp=None):
         _launch(tag, lambda: _lib.check(self.lib.dfno_dft_yzt_inv(
-            self.gp, _lib.ptr(xk_in), float(scale), _lib.ptr(out), _lib.stream_handle()), "dfno_dft_yzt_inv"))
+            gp or self.gp, _lib.ptr(xk_in), float(scale), _lib.ptr(out), _lib.stream_handle()), "dfno_dft_yzt_inv"))
+
+    # x-spectral stage by parts (pipelined blocks)
+    def xdft(self, gp, kx_in, scale, X, tag):
+        _launch(tag, lambda: _lib.check(self.lib.dfno_xdft(
+            gp, _lib.ptr(kx_in), float(scale), _lib.ptr(X), _lib.stream_handle()), "dfno_xdft"))
+
+    def xidft(self, gp, Y, scale, kx_out, tag):
+        _launch(tag, lambda: _lib.check(self.lib.dfno_xidft(
+            gp, _lib.ptr(Y), float(scale), _lib.ptr(kx_out), _lib.stream_handle()), "dfno_xidft"))
+
+    def xmix_fwd(self, X, w, Y):
+        _launch("xmix_fwd", lambda: _lib.check(self.lib.dfno_xmix_fwd(
+            self.gp, _lib.ptr(X), _lib.ptr(w), _lib.ptr(Y), _lib.stream_handle()), "dfno_xmix_fwd"))
+
+    def xmix_bwd(self, spec, D, w, gw, dX):
+        _launch("xmix_bwd", lambda: _lib.check(self.lib.dfno_xmix_bwd(
+            self.gp, _lib.ptr(spec), _lib.ptr(D), _lib.ptr(w), _lib.ptr(gw), _lib.ptr(dX), _lib.stream_handle()),
+            "dfno_xmix_bwd"))
+
+    def spectra(self) -> tuple:
+        """The two spectrum-sized halves of the x-spectral workspace (complex)."""
+        n = self.batch * self.config.hidden_channels * self.config.retained_x * self.kyl * \
+            self.config.retained_z * self.config.retained_t
+        flat = self.xspec_work.view(self.cplx)
+        return flat[:n].view(self.spec_shape), flat[n:2 * n].view(self.spec_shape)
+
+    def exchange_groups(self, comm: Communicator, send_of, recv_of, fwd: bool, label: str, after_each=None):
+        """Chunked repartition: for each channel group, after ``after_each(k)``
+        has enqueued its producer on the compute stream, the group's
+        all-to-all runs on the comm stream; returns one event per group that
+        the consumer of that group waits on.  Accounted as one repartition."""
+        S, C = torch.cuda.current_stream(), self.comm_stream
+        events, off_rank = [], 0
+        for k, grp in enumerate(self.groups):
+            if after_each is not None:
+                after_each(k, grp)
+            ready = torch.cuda.Event()
+            ready.record(S)
+            C.wait_event(ready)
+            with torch.cuda.stream(C):
+                sc, rc = (grp.xk_counts, grp.kx_counts) if fwd else (grp.kx_counts, grp.xk_counts)
+                off_rank += comm.exchange(send_of(grp), recv_of(grp), sc, rc, f"{label}.g{k}", record=False)
+                done = torch.cuda.Event()
+                done.record(C)
+            events.append(done)
+        comm.record_repartition(off_rank, self.buf_a.element_size())
+        return events
 
     def xspec_fwd(self, kx_in, w, spec, kx_out):
         _launch("xspec_fwd", lambda: _lib.check(self.lib.dfno_xspec_fwd_ws(
@@ -488,11 +592,11 @@ def _plan(config: FnoConfig, comm: Communicator, batch: int) -> _Plan:
         raise _lib.ExtensionMissingError("libdfno.so and a CUDA device are required (no CPU fallback)")
     check_envelope(config)
     device = comm.device if comm.device.type == "cuda" else _default_device()
-    key = (config, batch, str(device))
+    key = (config, batch, str(device), PIPELINE_GROUPS, PIPELINE_GROUPS_THREADED)
     plans = comm.__dict__.setdefault("_dfno_plans", {})
     plan = plans.get(key)
     if plan is None:
-        plan = _Plan(config, comm.rank, comm.world_size, batch, device)
+        plan = _Plan(config, comm.rank, comm.world_size, batch, device, threaded=comm.threaded)
         plans[key] = plan
     return plan
 
@@ -605,10 +709,43 @@ def _mixer_api(comm, x_local, w, activation, label):
     return DenseTensor(x_local.labels, post)
 
 
+def _block_forward_pipelined(comm, plan: _Plan, src: torch.Tensor, mode: int, w: torch.Tensor, label: str,
+                             want_spec: bool):
+    """_block_forward with the two repartitions chunked by channel group:
+
+        compute stream   yzt(g0) yzt(g1)           xdft(g0) xdft(g1) xmix xidft(g0) xidft(g1)            yzt^-1(g0) yzt^-1(g1)
+        comm stream              a2a(g0)  a2a(g1)                                   a2a'(g0)  a2a'(g1)
+
+    group k's all-to-all overlaps group k+1's DFT on either side of the
+    x-spectral stage (the contraction itself needs every channel)."""
+    S = torch.cuda.current_stream()
+    X0, Y = plan.spectra()
+    spec = torch.empty(plan.spec_shape, dtype=plan.cplx, device=plan.device) if want_spec else X0
+    x_of = lambda t, grp: t.view(-1)[grp.spec_off:]  # noqa: E731 - b = 1: channel slice of a spectrum
+    ev = plan.exchange_groups(
+        comm, lambda grp: grp.a, lambda grp: grp.b, True, f"{label}.fwd.x->ky",
+        after_each=lambda k, grp: plan.yzt_fwd(src[:, grp.c0:grp.c1], None, mode, 1.0, grp.a, tag="yzt_fwd.fwd",
+                                               gp=grp.gp))
+    for grp, e in zip(plan.groups, ev):
+        S.wait_event(e)
+        plan.xdft(grp.gp, grp.b, 1.0, x_of(spec, grp), "xdft.fwd")  # fft_x unnormalised (d/spectral.py:36)
+    plan.xmix_fwd(spec, w, Y)
+    ev = plan.exchange_groups(
+        comm, lambda grp: grp.c, lambda grp: grp.a, False, f"{label}.fwd.ky->x",
+        after_each=lambda k, grp: plan.xidft(grp.gp, x_of(Y, grp), 1.0 / plan.config.nx, grp.c, "xidft.fwd"))
+    pre = plan.empty_act(plan.config.hidden_channels)
+    for grp, e in zip(plan.groups, ev):
+        S.wait_event(e)
+        plan.yzt_inv(grp.a, 1.0 / plan.n_yzt, pre[:, grp.c0:grp.c1], tag="yzt_inv.fwd", gp=grp.gp)
+    return pre, (spec if want_spec else None)
+
+
 def _block_forward(comm, plan: _Plan, src: torch.Tensor, mode: int, w: torch.Tensor, label: str,
                    want_spec: bool):
     """fft_yzt -> truncate -> R(x->ky) -> fft_x -> truncate -> W -> pad ->
     ifft_x -> R(ky->x) -> pad -> ifft_yzt -> real  (reference fno.py:309-347)."""
+    if plan.groups:
+        return _block_forward_pipelined(comm, plan, src, mode, w, label, want_spec)
     plan.yzt_fwd(src, None, mode, 1.0, plan.buf_a, tag="yzt_fwd.fwd")
     kx_in = plan.x_to_ky(comm, f"{label}.fwd.x->ky")
     spec = torch.empty(plan.spec_shape, dtype=plan.cplx, device=plan.device) if want_spec else None
@@ -678,8 +815,30 @@ def _block_backward(comm, plan: _Plan, g: torch.Tensor, pre: Optional[torch.Tens
     """Adjoint chain (reference fno.py:445-464): fft_yzt/N_yzt -> truncate ->
     R(x->ky) -> fft_x/Nx -> truncate -> gW, dX -> pad -> ifft_x*Nx -> R(ky->x)
     -> pad -> ifft_yzt*N_yzt -> real."""
-    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a,
-                 tag="yzt_fwd.bwd" if mode == _lib.SRC_GRAD else "yzt_fwd.bwd_raw")
+    tag = "yzt_fwd.bwd" if mode == _lib.SRC_GRAD else "yzt_fwd.bwd_raw"
+    if plan.groups:  # chunked exchanges, as _block_forward_pipelined
+        S = torch.cuda.current_stream()
+        D, dX = plan.spectra()
+        x_of = lambda t, grp: t.view(-1)[grp.spec_off:]  # noqa: E731
+        ev = plan.exchange_groups(
+            comm, lambda grp: grp.a, lambda grp: grp.b, True, f"{label}.bwd.x->ky",
+            after_each=lambda k, grp: plan.yzt_fwd(
+                g[:, grp.c0:grp.c1], None if pre is None else pre[:, grp.c0:grp.c1], mode, 1.0 / plan.n_yzt, grp.a,
+                tag=tag, gp=grp.gp))
+        for grp, e in zip(plan.groups, ev):
+            S.wait_event(e)
+            plan.xdft(grp.gp, grp.b, 1.0 / plan.config.nx, x_of(D, grp), "xdft.bwd")  # fft_x / Nx (d/fno.py:450-452)
+        gw = torch.empty(plan.w_shape, dtype=plan.cplx, device=plan.device)
+        plan.xmix_bwd(spec, D, w, gw, dX)
+        ev = plan.exchange_groups(
+            comm, lambda grp: grp.c, lambda grp: grp.a, False, f"{label}.bwd.ky->x",
+            after_each=lambda k, grp: plan.xidft(grp.gp, x_of(dX, grp), 1.0, grp.c, "xidft.bwd"))
+        gin = plan.empty_act(plan.config.hidden_channels)
+        for grp, e in zip(plan.groups, ev):
+            S.wait_event(e)
+            plan.yzt_inv(grp.a, 1.0, gin[:, grp.c0:grp.c1], tag="yzt_inv.bwd", gp=grp.gp)
+        return gin, gw
+    plan.yzt_fwd(g, pre, mode, 1.0 / plan.n_yzt, plan.buf_a, tag=tag)
     kx_in = plan.x_to_ky(comm, f"{label}.bwd.x->ky")
     gw = torch.empty(plan.w_shape, dtype=plan.cplx, device=plan.device)
     plan.xspec_bwd(kx_in, spec, w, gw, plan.buf_c)

@@ -150,7 +150,11 @@ def test_c3_128cubed(ranks):
     _free()
 
 
-def test_c4_co2_grid_p8_geometry():
+@pytest.mark.parametrize("groups", [1, 2], ids=["unsplit", "pipelined"])
+def test_c4_co2_grid_p8_geometry(groups, monkeypatch):
+    from paper_2211_12709_b200 import fno as F
+
+    monkeypatch.setattr(F, "PIPELINE_GROUPS_THREADED", groups)
     # 262 x 118 x 64 x 86 at P = 8: x slabs 33 x 6 + 32 x 2, ky pencils of 2,
     # Nt = 86 and Ny = 118 (not multiples of 4 / 8)
     config = _config((262, 118, 64, 86), (8, 8, 8, 8), 8, 2, 8)

@@ -86,9 +86,19 @@ def load(golden_dir, name):
     return d, meta, [d[f"w{i}"] for i in range(meta["blocks"])]
 
 
+@pytest.fixture(params=[1, 2], ids=["unsplit", "pipelined"])
+def pipeline(request, monkeypatch):
+    """Thread worlds run both the unsplit exchanges and the channel-group
+    pipelined ones that process-group (NCCL) worlds use by default."""
+    from paper_2211_12709_b200 import fno as F
+
+    monkeypatch.setattr(F, "PIPELINE_GROUPS_THREADED", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name,ranks", GOLDEN)
 @pytest.mark.parametrize("dtype", ["real64", "real32"])
-def test_forward_backward_match_reference_goldens(golden_dir, name, ranks, dtype):
+def test_forward_backward_match_reference_goldens(golden_dir, name, ranks, dtype, pipeline):
     d, meta, blocks = load(golden_dir, name)
     config = make_config(meta, ranks, dtype)
     y, gx, gwe, gwd, gws, counters, _ = run_fwd_bwd(config, d["x"], d["we"], d["wd"], blocks)
@@ -136,7 +146,7 @@ def _random_case(grid, modes, c, blocks, seed, act="gelu", batch=1):
 
 @pytest.mark.parametrize("dtype", ["real32", "real64"])
 @pytest.mark.parametrize("ranks", [1, 4])
-def test_production_modes_against_oracle(dtype, ranks):
+def test_production_modes_against_oracle(dtype, ranks, pipeline):
     # production mode counts (m = 8 on every dim, r = 16) and width 20 on a
     # grid the oracle finishes in seconds; exercises the tcgen05 DFT path at fp32
     meta, x, we, wd, blocks = _random_case((32, 32, 32, 16), (8, 8, 8, 8), 20, 2, seed=3)
@@ -154,7 +164,7 @@ def test_production_modes_against_oracle(dtype, ranks):
 
 
 @pytest.mark.parametrize("dtype", ["real32", "real64"])
-def test_c4_like_odd_extents_against_oracle(dtype):
+def test_c4_like_odd_extents_against_oracle(dtype, pipeline):
     # non-multiple-of-8 extents like the CO2 grid (262x118x64x86), scaled down
     meta, x, we, wd, blocks = _random_case((13, 118 // 4, 16, 86 // 4), (4, 8, 8, 8), 6, 2, seed=9, batch=2)
     for ranks in (1, 3):
@@ -201,7 +211,7 @@ def test_determinism_bitwise():
         assert np.array_equal(u, v)
 
 
-def test_replicated_mixer_grads_bit_identical_across_ranks():
+def test_replicated_mixer_grads_bit_identical_across_ranks(pipeline):
     meta, x, we, wd, blocks = _random_case((12, 8, 8, 4), (2, 2, 2, 2), 3, 1, seed=4)
     config = make_config(meta, 3, "real32")
     res = run_fwd_bwd(config, x, we, wd, blocks)[6]
