@@ -558,7 +558,7 @@ def run_single_gpu_config(args):
     # busiest rank's geometry (x_r = 33 / ky_r = 2 at C4, every rank at C3)
     xl = max(v[0] for v in times["xl"].values())
     kyl = max(v[1] for v in times["xl"].values())
-    G = min(F.PIPELINE_GROUPS, CHANNELS) if ranks > 1 else 1  # channel groups of the pipelined exchanges
+    G = min(F.PIPELINE_GROUPS_THREADED, CHANNELS) if ranks > 1 else 1  # channel groups (thread ranks)
     ab = alg_bytes(cfg, xl, kyl, ranks, G)
     # mean per-launch bytes over ranks (uneven x slabs)
     ab_mean = {k: sum(alg_bytes(cfg, v[0], v[1], ranks, G)[k] for v in times["xl"].values()) / ranks for k in ab}

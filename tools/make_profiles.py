@@ -21,6 +21,9 @@ CAPTURES = {
     "yzt_fwd_act": ["yzt_fwd.fwd"], "yzt_fwd_grad": ["yzt_fwd.bwd"], "yzt_inv": ["yzt_inv.fwd", "yzt_inv.bwd"],
     "mix_bwd": ["mix_bwd.dec", "mix_bwd.enc"], "mix_fwd": ["mix_fwd.enc"], "xmix": [], "xmix_bwd": [], "xdft": [],
     "xidft": [],
+    # round-2 capture names (tools/gpu_r02_evidence.sh)
+    "fwd_c2": ["yzt_fwd.fwd"], "inv_c2": ["yzt_inv.fwd", "yzt_inv.bwd"], "mixbwd_c2": ["mix_bwd.dec", "mix_bwd.enc"],
+    "xdft_c2": [], "xidft_c2": [],
 }
 
 
