@@ -64,7 +64,7 @@ __host__ __device__ inline XLay make_xlay(int nx, int xmax, int xcnt, bool red) 
   L.nch = (xcnt + kC - 1) / kC;
   int o = 0;
   L.off_ph = o; o += 16 * nx;                         // float4 (cos hi, cos lo, sin hi, sin lo) of 2 pi j / N_x
-  L.off_rows = o; o += 8 * nch_max * kC;              // KX row offset of each x of the range, per tile
+  L.off_rows = o; o += 2 * 8 * nch_max * kC;          // per x of the range: KX row offset at (b c) = 0, (b c) stride
   o = (o + 1023) & ~1023;
   L.off_b = o; o += nch_max * kBChunk;
   L.off_red = o; o += red ? kT * 33 * 4 : 0;         // cluster reduction: [mode][32 (+1)] partial sums
@@ -112,6 +112,19 @@ __device__ void build_twiddles(const dfno_geom& g, const XLay& L, unsigned char*
   }
 }
 
+// KX layout (common.cuh kx_row): row(bc, x) = r0[x] + bc * rs[x], tables for
+// the CTA's x range built once (no per-tile row table, no per-tile barrier)
+__device__ void build_rows(const dfno_geom& g, long long* r0, long long* rs, int x0, int xcnt) {
+  const long long mloc = (long long)ky_local(g) * g.rz * g.rt;
+  for (int i = threadIdx.x; i < xcnt; i += blockDim.x) {
+    const int x = x0 + i;
+    const int p = x_owner(g, x);
+    const long long xp = g.x_starts[p + 1] - g.x_starts[p];
+    r0[i] = kx_row(g, 0, 0, x);
+    rs[i] = xp * mloc;
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -140,7 +153,10 @@ __global__ void __launch_bounds__(kT, 2) k_xdft_tc(const dfno_geom g, const floa
   tc::fence_after();
   const uint32_t tmem = tmem_base, lane_off = (uint32_t)(32 * warp) << 16;
   const uint32_t cA = 0, cD = 128;  // A: 2 x (hi 32 | lo 32); D: 2 x 64
-  long long* rows = reinterpret_cast<long long*>(smem + L.off_rows);
+  long long* r0 = reinterpret_cast<long long*>(smem + L.off_rows);
+  long long* rs = r0 + L.nch * kC;
+  build_rows(g, r0, rs, x0, L.xcnt);
+  __syncthreads();
   const uint32_t sb = tc::smem_u32(smem + L.off_b);
   const uint32_t id64 = tc::idesc_tf32(128, 64), id32 = tc::idesc_tf32(128, 32);
 
@@ -149,22 +165,21 @@ __global__ void __launch_bounds__(kT, 2) k_xdft_tc(const dfno_geom g, const floa
   const long long ntiles = (long long)g.batch * g.c * mtiles;
   const long long walkers = gridDim.x / xs, w0 = blockIdx.x / xs;
   int q = 0;  // running chunk counter: A / D buffer parity
+  // the loads run one chunk ahead, across tile boundaries
+  float2 z[kC];
+  auto fetch = [&](long long tile, int ch) {
+    const long long bc = tile / mtiles, m = (tile - bc * mtiles) * kT + tid;
+    const bool ok = tile < ntiles && m < mloc;
+#pragma unroll
+    for (int i = 0; i < kC; ++i) {
+      const int xi = ch * kC + i;
+      z[i] = (ok && xi < L.xcnt) ? __ldcs(kx_in + r0[xi] + bc * rs[xi] + m) : make_float2(0.f, 0.f);
+    }
+  };
+  fetch(w0, 0);
   for (long long tile = w0; tile < ntiles; tile += walkers) {
     const long long bc = tile / mtiles, m = (tile - bc * mtiles) * kT + tid;
-    const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
     const bool ok = m < mloc;
-    __syncthreads();  // previous tile's D read-out and row table use are done
-    for (int i = tid; i < L.xcnt; i += kT) rows[i] = kx_row(g, bb, c, x0 + i);
-    __syncthreads();
-    float2 z[kC];
-    auto fetch = [&](int ch) {
-#pragma unroll
-      for (int i = 0; i < kC; ++i) {
-        const int xi = ch * kC + i;
-        z[i] = (ok && xi < L.xcnt) ? __ldcs(kx_in + rows[xi] + m) : make_float2(0.f, 0.f);
-      }
-    };
-    fetch(0);
     // Each chunk accumulates in a fresh TMEM accumulator (double-buffered with
     // A) and the chunk sums are added in registers with round-to-nearest
     // fp32 adds: the tensor core's accumulator adds truncate, and a long
@@ -189,7 +204,8 @@ __global__ void __launch_bounds__(kT, 2) k_xdft_tc(const dfno_geom g, const floa
       float h[32], l[32];
 #pragma unroll
       for (int i = 0; i < kC; ++i) tc::split_hl2(z[i], h[2 * i], h[2 * i + 1], l[2 * i], l[2 * i + 1]);
-      if (ch + 1 < L.nch) fetch(ch + 1);
+      if (ch + 1 < L.nch) fetch(tile, ch + 1);
+      else fetch(tile + walkers, 0);
       const int ab = q & 1;
       // buffer ab (A and D) was last used by chunk q - 2, drained by this
       // thread one iteration ago (or in the previous tile)
@@ -273,7 +289,10 @@ __global__ void __launch_bounds__(kT, 2) k_xidft_tc(const dfno_geom g, const flo
   tc::fence_after();
   const uint32_t tmem = tmem_base, lane_off = (uint32_t)(32 * warp) << 16;
   const uint32_t cA = 0, cD = 64;  // A: hi 32 | lo 32; D: 2 x 64
-  long long* rows = reinterpret_cast<long long*>(smem + L.off_rows);
+  long long* r0t = reinterpret_cast<long long*>(smem + L.off_rows);
+  long long* rst = r0t + L.nch * kC;
+  build_rows(g, r0t, rst, x0, L.xcnt);
+  __syncthreads();
   const uint32_t sb = tc::smem_u32(smem + L.off_b);
   const uint32_t id64 = tc::idesc_tf32(128, 64), id32 = tc::idesc_tf32(128, 32);
 
@@ -295,23 +314,26 @@ __global__ void __launch_bounds__(kT, 2) k_xidft_tc(const dfno_geom g, const flo
     }
     tc::commit(&dfull[db]);
   };
+  // the next tile's Y is loaded while this tile's chunks run
+  float2 yv[16];
+  auto load_y = [&](long long tile) {
+    const long long bc = tile / mtiles, m = (tile - bc * mtiles) * kT + tid;
+    const bool ok = tile < ntiles && m < mloc;
+    const float2* src = Y + (bc * g.rx) * mloc + m;
+#pragma unroll
+    for (int kx = 0; kx < 16; ++kx)
+      yv[kx] = (ok && kx < g.rx) ? __ldg(src + (long long)kx * mloc) : make_float2(0.f, 0.f);
+  };
+  load_y(w0);
   for (long long tile = w0; tile < ntiles; tile += walkers) {
     const long long bc = tile / mtiles, m = (tile - bc * mtiles) * kT + tid;
-    const int c = (int)(bc % g.c), bb = (int)(bc / g.c);
     const bool ok = m < mloc;
     float h[32], l[32];
-    {
-      const float2* src = Y + (bc * g.rx) * mloc + m;
 #pragma unroll
-      for (int kx = 0; kx < 16; ++kx) {
-        const float2 y = (ok && kx < g.rx) ? __ldg(src + (long long)kx * mloc) : make_float2(0.f, 0.f);
-        tc::split_hl2(y, h[2 * kx], h[2 * kx + 1], l[2 * kx], l[2 * kx + 1]);
-      }
-    }
-    // the previous tile's MMAs (which read A) are done once its last
-    // accumulator was drained: every thread waited on that dfull
-    __syncthreads();
-    for (int i = tid; i < L.xcnt; i += kT) rows[i] = kx_row(g, bb, c, x0 + i);
+    for (int kx = 0; kx < 16; ++kx) tc::split_hl2(yv[kx], h[2 * kx], h[2 * kx + 1], l[2 * kx], l[2 * kx + 1]);
+    load_y(tile + walkers);
+    // the previous tile's MMAs (which read A) are done: this thread waited
+    // on that tile's last accumulator, committed after all of them
     tc::tmem_st32(tmem + cA + lane_off, h);
     tc::tmem_st32(tmem + cA + 32 + lane_off, l);
     tc::tmem_st_wait();
@@ -338,7 +360,7 @@ __global__ void __launch_bounds__(kT, 2) k_xidft_tc(const dfno_geom g, const flo
           if (xi < L.xcnt) {
             const float re = __uint_as_float(r0[i]) + __uint_as_float(r1[i]);
             const float im = __uint_as_float(r0[16 + i]) + __uint_as_float(r1[16 + i]);
-            __stcs(kx_out + rows[xi] + m, make_float2(s2 * re, s2 * im));
+            __stcs(kx_out + r0t[xi] + bc * rst[xi] + m, make_float2(s2 * re, s2 * im));
           }
         }
       }
