@@ -590,6 +590,21 @@ def run_single_gpu_config(args):
     print(json.dumps(result), flush=True)
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+CALIBRATION = ("the real reference (distfno scale --transport proc, P = 8, C1) is 1.69x slower than this port on "
+               "the same cores (profiles/r02_reference_calibration_32x32x32x16_P8.json), so this value overstates "
+               "the reference's throughput")
+
+
 def cpu_baseline(grid, ranks, steps):
     from oracle import cpu_baseline as cb
 
@@ -601,7 +616,7 @@ def cpu_baseline(grid, ranks, steps):
             "sample": (f"one rank's fwd+bwd of a {ranks}-way x decomposition of the {grid} grid (reference's staged "
                        f"numpy pipeline, oracle/cpu_baseline.py), {cores} processes in parallel, 1 thread each; "
                        f"rank time {statistics.median(per_rank):.2f} s, job time = rank time x {ranks}/{cores}"),
-            "job_seconds_per_sample": round(t / units, 3)}
+            "job_seconds_per_sample": round(t / units, 3), "cpu_model": cpu_model(), "calibration": CALIBRATION}
 
 
 def run_reference(args):
@@ -627,7 +642,8 @@ def run_reference(args):
         "config": {"workload": wname, "grid": list(grid), "channels": CHANNELS, "modes": list(MODES),
                    "blocks": BLOCKS, "batch": 1, "parallelism": f"cpu {cores} processes"},
         "cpu_baseline": {"value": round(value, 6), "unit": "samples/s", "cores": cores, "kind": "port",
-                         "sample": f"per step: one rank's fwd+bwd of a {ranks}-way decomposition x {ranks}/{cores}"},
+                         "sample": f"per step: one rank's fwd+bwd of a {ranks}-way decomposition x {ranks}/{cores}",
+                         "cpu_model": cpu_model(), "calibration": CALIBRATION},
         "e2e": {"value": round(value, 6), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

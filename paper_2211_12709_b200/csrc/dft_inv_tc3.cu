@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base;
+#ifdef DFNO_WAIT_PROF
+  const long long t_start = clock64();
+#endif
   const uint32_t qoff = (uint32_t)(32 * (warp & 3)) << 16;
 
   const int slabs = g.batch * g.c * XL;
@@ -499,6 +502,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
     }
   }
+#ifdef DFNO_WAIT_PROF
+  tc::prof_life(t_start);
+#endif
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -533,6 +539,16 @@ int smem_cap_3() {
 }
 
 }  // namespace
+
+#ifdef DFNO_WAIT_PROF
+extern "C" int dfno_debug_wait_prof_inv(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, tc::g_wait_prof, sizeof(tc::g_wait_prof));
+  static unsigned long long zero[tc::kProfCtas][tc::kProfWarps][2];
+  cudaMemcpyToSymbol(tc::g_wait_prof, zero, sizeof(zero));
+  return DFNO_OK;
+}
+#endif
 
 int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
   if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;

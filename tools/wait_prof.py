@@ -17,6 +17,7 @@ from paper_2211_12709_b200 import _lib  # noqa: E402
 import time_kernel  # noqa: E402
 
 ROLES = {0: "conv", 8: "T-epi", 16: "Z-epi", 20: "TMA", 21: "issT0", 22: "issT1", 23: "issZ", 24: "issY", 25: "twid"}
+ROLES_INV = {0: "front", 4: "T-epi", 8: "O-epi", 16: "issY", 17: "issT", 18: "issZ", 20: "loader", 21: "twid"}
 
 
 def main(which):
@@ -24,7 +25,9 @@ def main(which):
     time_kernel.main(which, 3, grid=grid)  # warm-up + timing print
     lib = _lib.load()
     buf = np.zeros((160, 32, 2), dtype=np.uint64)
-    f = lib.dfno_debug_wait_prof_fwd
+    inv = which.startswith("yzt_inv")
+    f = lib.dfno_debug_wait_prof_inv if inv else lib.dfno_debug_wait_prof_fwd
+    roles = ROLES_INV if inv else ROLES
     f(buf.ctypes.data_as(ctypes.c_void_p))  # clear
     time_kernel.main(which, 1, grid=grid)
     f(buf.ctypes.data_as(ctypes.c_void_p))
@@ -34,9 +37,9 @@ def main(which):
     for w in range(32):
         if not act[w]:
             continue
-        role = max(k for k in ROLES if k <= w)
+        role = max(k for k in roles if k <= w)
         share = wait[:, w].sum() / max(life[:, w].sum(), 1)
-        print(f"  warp {w:2d} {ROLES[role]:6s} wait {100 * share:5.1f}%")
+        print(f"  warp {w:2d} {roles[role]:6s} wait {100 * share:5.1f}%")
 
 
 if __name__ == "__main__":
