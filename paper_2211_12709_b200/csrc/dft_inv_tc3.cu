@@ -52,7 +52,7 @@ constexpr int kAYPlane3 = 16 * 1024;          // 128 rows x K 32 fp32
 constexpr int kBYPlane3 = 4 * 1024;           // one pass: 32 rows (re | im, y 16) x K 32
 constexpr int kBlk3 = 16 * 1024;              // one t or z block of twiddles: 64 rows x K 32, hi + lo
 constexpr int kS1 = 20;                       // stash1 kt pitch (floats)
-constexpr int kS2 = 65;                       // stash2 row pitch (floats)
+constexpr int kS2 = 68;                       // stash2 row pitch (floats): 16-byte rows, conflict-free STS.128
 
 // TMEM columns: D_Y 2 x 32 | A_T 64 | D_T 2 x 64 | A_Z 2 x 64 | D_Z 2 x 64
 constexpr uint32_t jDY = 0, jAT = 64, jDT = 128, jAZ = 256, jDZ = 384;
@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       tc::mbar_arrive(&dt_empty[b]);
       float* dst = s2 + (yl * 16 + kz) * kS2;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) dst[c] = __uint_as_float(u[c]);
+      for (int c = 0; c < 64; c += 4)
+        *reinterpret_cast<float4*>(dst + c) = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]),
+                                                          __uint_as_float(u[c + 2]), __uint_as_float(u[c + 3]));
       tc::named_sync(2, 128);
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
@@ -313,9 +315,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const float* src = s2 + ((4 * h + q) * 16) * kS2 + lane;  // A_Z row (y_l = 4h + q, t = lane)
         float hr[32], lr[32];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          tc::split_hl(src[k * kS2], hr[k], lr[k]);                 // kz re
-          tc::split_hl(src[k * kS2 + 32], hr[16 + k], lr[16 + k]);  // kz im
+        for (int k = 0; k < 16; k += 2) {
+          tc::split_hl2(make_float2(src[k * kS2], src[(k + 1) * kS2]), hr[k], hr[k + 1], lr[k], lr[k + 1]);  // kz re
+          tc::split_hl2(make_float2(src[k * kS2 + 32], src[(k + 1) * kS2 + 32]), hr[16 + k], hr[17 + k], lr[16 + k],
+                        lr[17 + k]);  // kz im
         }
         tc::tmem_st32(tmem + jAZ + 64 * ab + qoff, hr);
         tc::tmem_st32(tmem + jAZ + 64 * ab + 32 + qoff, lr);
