@@ -303,13 +303,15 @@ def run_ours(args):
     if world > 1:
         orig_exchange = comm.exchange
 
-        def timed_exchange(send, recv, send_counts, recv_counts, label=""):
+        def timed_exchange(send, recv, send_counts, recv_counts, label="", record=True):
+            # events on the current stream: the comm stream of the pipelined exchanges
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            orig_exchange(send, recv, send_counts, recv_counts, label)
+            n = orig_exchange(send, recv, send_counts, recv_counts, label, record)
             e.record()
             a2a["events"].append((s, e))
             a2a["bytes"] += sum(n for p, n in enumerate(send_counts) if p != rank) * send.element_size()
+            return n
 
         comm.exchange = timed_exchange
     clocks = ClockSampler(local)

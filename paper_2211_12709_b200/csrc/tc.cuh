@@ -230,10 +230,14 @@ __device__ __forceinline__ void prof_life(long long t_start) {
 #define DFNO_PROF_WAIT
 #endif
 
+#ifndef DFNO_WAIT_BACKOFF_NS
+#define DFNO_WAIT_BACKOFF_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   DFNO_PROF_WAIT;
   uint32_t n = 0;
   while (!(DFNO_WAIT_HINT ? mbar_try_hint(bar, parity) : mbar_try(bar, parity))) {
+    if (DFNO_WAIT_BACKOFF_NS) __nanosleep(DFNO_WAIT_BACKOFF_NS);
     if (++n > (1u << 28)) __trap();
   }
 }
