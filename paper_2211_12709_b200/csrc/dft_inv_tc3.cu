@@ -107,7 +107,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
 
 }  // namespace
 
-template <bool FAST>  // FAST: N_z == 64 and N_t == 32 (compile-time store offsets)
+// NT > 0: N_t known at compile time (32 for the 3-D Navier-Stokes grids, 86
+// for the CO2 grid), so the output epilogue's z-strided stores use immediate
+// offsets; ZFULL: N_z % 64 == 0 (no partial z block).  NT = 0: generic.
+template <int NT, bool ZFULL>
 __global__ void __launch_bounds__(kThreads3, 1)
     k_yzt_inv_tc3(const dfno_geom g, const float2* __restrict__ in, float* __restrict__ out, float scale, int nby) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -116,7 +119,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   __shared__ uint64_t dt_full[2], dt_empty[2], az_full[2], az_empty[2], dz_full[2], dz_empty[2];
   __shared__ uint32_t tmem_base;
 
-  const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
+  const int Ny = g.ny, Nz = g.nz, Nt = NT > 0 ? NT : g.nt;
+  constexpr bool FAST = NT == 32;
   const int XL = x_local(g);
   const Lay3 L = make_lay3(Ny, Nz, Nt, nby);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -353,10 +357,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::tmem_ld_wait();
         tc::fence_before();
         tc::mbar_arrive(&dz_empty[k]);
-        if (FAST) {
+        if (FAST && Nz == 64) {
           if (y < Ny) {
 #pragma unroll
             for (int z = 0; z < 64; ++z) __stcs(o + z * 32, __uint_as_float(w[z]));
+          }
+        } else if (NT > 0 && ZFULL) {
+          if (y < Ny && t < Nt) {
+            float* oz = o + (long long)(64 * zo) * Nt;
+#pragma unroll
+            for (int z = 0; z < 64; ++z) __stcs(oz + z * Nt, __uint_as_float(w[z]));
           }
         } else if (y < Ny && t < Nt) {
           float* oz = o + (long long)(64 * zo) * Nt;
@@ -559,8 +569,10 @@ int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cud
   Lay3 L = make_lay3(g.ny, g.nz, g.nt, 2);
   if (L.total > smem_cap_3()) L = make_lay3(g.ny, g.nz, g.nt, 1);
   if (L.total > smem_cap_3()) return DFNO_ERR_UNSUPPORTED;
-  const bool fast = g.nz == 64 && g.nt == 32;
-  auto kern = fast ? k_yzt_inv_tc3<true> : k_yzt_inv_tc3<false>;
+  const bool zfull = g.nz % 64 == 0;
+  auto kern = (g.nt == 32 && zfull)        ? k_yzt_inv_tc3<32, true>
+              : (g.nt == 86 && zfull)      ? k_yzt_inv_tc3<86, true>
+                                           : k_yzt_inv_tc3<0, false>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
