@@ -279,7 +279,7 @@ def run_ours(args):
     # kernels and buffers, captured after an eager warm-up); the eager loop
     # below times the same step launch by launch for the kernel table
     graph = P.FwdBwdGraph(comm, x, params, cfg) if world == 1 else None
-    ms_graph = None
+    ms_graph = ms_fwd = None
     if graph is not None:
         for _ in range(max(1, args.warmup)):
             graph.replay()
@@ -295,6 +295,19 @@ def run_ours(args):
         barrier()
         clock_info_g = clocks_g.stop()
         ms_graph = g0.elapsed_time(g1) / args.steps
+        # forward alone (the reference scale driver's efficiency column, d/cli.py:171-178)
+        fgraph = P.FwdBwdGraph(comm, x, params, cfg, backward=False)
+        for _ in range(max(1, args.warmup)):
+            fgraph.replay()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            fgraph.replay()
+        f1.record()
+        barrier()
+        ms_fwd = f0.elapsed_time(f1) / args.steps
+        del fgraph
 
     timer = KernelTimer()
     F.set_kernel_timer(timer)
@@ -448,6 +461,8 @@ def run_ours(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(ms_max, 4),
+        "fwd_only": ({"value": round(world * 1e3 / ms_fwd, 3), "unit": "samples/s", "ms_per_step": round(ms_fwd, 4)}
+                     if ms_fwd else None),
         "step_mode": ("one CUDA graph per step (P.FwdBwdGraph); eager launch-by-launch step "
                       f"{ms_eager:.4f} ms, which also gives the kernel table") if ms_graph is not None else "eager",
         "higher_is_better": True,

@@ -40,7 +40,7 @@ class FwdBwdGraph:
     replay."""
 
     def __init__(self, comm: Communicator, x: DenseTensor, params: FnoParams, config: FnoConfig,
-                 grad: Optional[Callable[[DenseTensor], DenseTensor]] = None):
+                 grad: Optional[Callable[[DenseTensor], DenseTensor]] = None, backward: bool = True):
         if comm.threaded and comm.world_size > 1:
             raise DimensionMismatchError("the thread backend synchronises ranks on the host; it cannot be captured")
         if not x.data.is_cuda:
@@ -48,6 +48,7 @@ class FwdBwdGraph:
         self.comm, self.params, self.config = comm, params, config
         self.x = x
         self._grad = grad or (lambda y: y)
+        self._backward = backward  # False: forward only (the reference's scale-driver column)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # eager warm-up: plans, workspaces, broadcast headers
@@ -58,6 +59,8 @@ class FwdBwdGraph:
             self.y, self.gx, self.grads = self._step()
 
     def _step(self):
+        if not self._backward:
+            return fno_forward(self.comm, self.x, self.params, self.config), None, None
         cache = ForwardCache()
         y = fno_forward(self.comm, self.x, self.params, self.config, cache)
         gx, grads = fno_backward(self.comm, self._grad(y), self.params, self.config, cache)

@@ -122,3 +122,16 @@ def test_truncate_pad_adjoint_host_tensors():
     lhs = np.vdot(P.truncate_modes(x, spec).numpy(), y.numpy())
     rhs = np.vdot(x.numpy(), P.pad_modes(y, spec, {"ky": 9, "kz": 6}).numpy())
     assert abs(lhs - rhs) < 1e-12 * max(abs(lhs), 1)
+
+
+def test_channel_envelope_rejected_before_any_kernel():
+    # the mixer backward / spectral contraction keep a channel row per thread:
+    # widths above 32 are refused when the plan is built, not mid-backward
+    import paper_2211_12709_b200 as P
+    from paper_2211_12709_b200 import fno as F
+
+    ok = P.FnoConfig(8, 8, 8, 4, 32, 32, 32, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real32", 1)
+    F.check_envelope(ok)
+    wide = P.FnoConfig(8, 8, 8, 4, 3, 3, 40, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real32", 1)
+    with pytest.raises(P.DimensionMismatchError, match="hidden_channels"):
+        F.check_envelope(wide)
