@@ -13,10 +13,12 @@
 //
 //   producer       4-D tensor-map loads (SWIZZLE_128B) of each tile into a
 //                  shared-memory ring (src, and pre in backward mode).  TMA
-//                  needs 16-byte aligned row starts, so for N_t % 4 != 0 (the
-//                  CO2 grid's N_t = 86) two warps write the same swizzled
-//                  tiles with 8- or 4-byte cp.async instead, zero-filling
-//                  outside the grid (about half the TMA path's bandwidth)
+//                  needs 16-byte aligned row starts: for N_t % 4 == 2 (the CO2
+//                  grid's N_t = 86) two unswizzled maps load the even and the
+//                  odd z rows (row pairs are aligned; the odd map starts two
+//                  floats early), 36-float lines read with 8-byte loads; for
+//                  odd N_t two warps write the swizzled tiles with 4-byte
+//                  cp.async instead, zero-filling outside the grid
 //   twiddle warp   builds the stage-Y operand of each y chunk (hi / lo planes,
 //                  K = 8 y re | im) from an fp64 phase table into a 2-slot
 //                  ring, so no N_y-sized table is resident
@@ -65,6 +67,11 @@ constexpr int kTwW = 25;                  // stage-Y twiddle builder
 constexpr int kWarps = 26;
 constexpr int kThreads2 = kWarps * 32;
 constexpr int kTileBytes = 128 * 32 * 4;            // 128 rows x 32 t fp32
+// N_t % 4 == 2 (the CO2 grid's 86): even and odd z rows come from two TMA maps
+// (no swizzle) with 36-float rows; an odd row's data starts 8 bytes in
+constexpr int kPairRow = 36 * 4;
+constexpr int kPairHalf = 64 * kPairRow;            // one parity: 8 y x 8 z pairs
+constexpr int kPairTile = 2 * kPairHalf;
 constexpr int kScratchWarp = 2 * 16 * 17 * 4;       // [yy][kt][z (+1)], one part (re / im) at a time
 constexpr int kStashBytes = 2 * 16 * 16 * 9 * 4;    // [part][kz][kt][y (+1)]
 constexpr int kAYPlane = 16 * 512;                  // 128 rows x K 16, SBO 512 (one hi or lo plane of one tile)
@@ -79,11 +86,11 @@ struct Lay {
   int nyc, nzb, ntb;            // y chunks (8), z blocks (16), t blocks (32)
   int kt_tot, kz_tot;           // K extents of the resident twiddle operands
   int sbo_t, sbo_z;
-  int off_ring, off_bt, off_bz, off_by, off_ph, off_scr, off_stash, off_ay, total;
+  int off_ring, off_bt, off_bz, off_by, off_ph, off_scr, off_stash, off_ay, total, tile;
   int stages, srcs;             // ring depth, tiles per stage (1 or 2)
 };
 
-__host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int smem_cap) {
+__host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int smem_cap, int tile = kTileBytes) {
   Lay L;
   L.nyc = (ny + 7) / 8;
   L.nzb = (nz + 15) / 16;
@@ -103,11 +110,12 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   o = (o + 1023) & ~1023;
   L.off_ay = o; o += kAYBytes;
   L.off_ring = o;
-  const int stage = srcs * kTileBytes;
+  const int stage = srcs * tile;
   int s = (smem_cap - o) / stage;
   // two converter sets need an even depth: ring stage s always holds tiles of parity s & 1
   s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);
   L.stages = s;
+  L.tile = tile;
   L.total = o + s * stage;
   return L;
 }
@@ -156,8 +164,10 @@ struct GroupIdx {
 template <int MODE, int ACT>
 __global__ void __launch_bounds__(kThreads2, 1)
     k_yzt_fwd_tc2(const dfno_geom g, const __grid_constant__ CUtensorMap tm_src,
-                  const __grid_constant__ CUtensorMap tm_pre, const float* __restrict__ srcp,
-                  const float* __restrict__ prep, int use_ca, float scale, float2* __restrict__ out, int smem_cap) {
+                  const __grid_constant__ CUtensorMap tm_pre, const __grid_constant__ CUtensorMap tm_src_odd,
+                  const __grid_constant__ CUtensorMap tm_pre_odd, const float* __restrict__ srcp,
+                  const float* __restrict__ prep, int use_ca, int zpair, float scale, float2* __restrict__ out,
+                  int smem_cap) {
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -168,7 +178,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
   const int Ny = g.ny, Nz = g.nz, Nt = g.nt;
   const int XL = x_local(g);
-  const Lay L = make_lay(Ny, Nz, Nt, GRAD ? 2 : 1, smem_cap);
+  const Lay L = make_lay(Ny, Nz, Nt, GRAD ? 2 : 1, smem_cap, zpair ? kPairTile : kTileBytes);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* bt = smem + L.off_bt;
   unsigned char* bz = smem + L.off_bz;
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const int s = j % S, n = j / S;
       const long long slab = (long long)blockIdx.x + (long long)gi.slab_g * gridDim.x;
       tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
-      unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
+      unsigned char* dst = smem + L.off_ring + s * L.srcs * L.tile;
 #pragma unroll 1
       for (int si = 0; si < L.srcs; ++si) {
         const float* base = (si == 0 ? srcp : prep) + slab * slab_elems;
@@ -321,21 +331,37 @@ __global__ void __launch_bounds__(kThreads2, 1)
     for (int i = set; set < kSets && i < n_tiles; i += kSets) {
       const int s = i % S, n = i / S;
       tc::mbar_wait_lazy(&full[s], n & 1, 32);
-      const unsigned char* rowp = smem + L.off_ring + s * L.srcs * kTileBytes + r * 128;
+      const unsigned char* ring = smem + L.off_ring + s * L.srcs * L.tile;
+      const unsigned char* rowp = ring + r * 128;
       const int b = i & 1;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float h[16], l[16];
+        if (zpair) {
+          // row (y, z): parity half of the tile, (y, z / 2) line of 36 floats,
+          // odd rows 8 bytes in; eight-byte loads (conflict-free: lanes
+          // alternate parity, z pairs step the bank by 4)
+          const int zl = r & 15;
+          const unsigned char* prow = ring + (zl & 1) * kPairHalf + ((r >> 4) * 8 + (zl >> 1)) * kPairRow + (zl & 1) * 8;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int c = 4 * half + c4;
-          const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
-          float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-          if constexpr (GRAD) p = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
-          const float2 a = conv2<MODE, ACT>(make_float2(q.x, q.y), make_float2(p.x, p.y));
-          const float2 b = conv2<MODE, ACT>(make_float2(q.z, q.w), make_float2(p.z, p.w));
-          tc::split_hl2(a, h[4 * c4], h[4 * c4 + 1], l[4 * c4], l[4 * c4 + 1]);
-          tc::split_hl2(b, h[4 * c4 + 2], h[4 * c4 + 3], l[4 * c4 + 2], l[4 * c4 + 3]);
+          for (int c2 = 0; c2 < 8; ++c2) {
+            const float2 q = *reinterpret_cast<const float2*>(prow + (16 * half + 2 * c2) * 4);
+            float2 pp = make_float2(0.f, 0.f);
+            if constexpr (GRAD) pp = *reinterpret_cast<const float2*>(prow + L.tile + (16 * half + 2 * c2) * 4);
+            tc::split_hl2(conv2<MODE, ACT>(q, pp), h[2 * c2], h[2 * c2 + 1], l[2 * c2], l[2 * c2 + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int c = 4 * half + c4;
+            const float4 q = *reinterpret_cast<const float4*>(rowp + ((c ^ sw) << 4));
+            float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+            if constexpr (GRAD) p = *reinterpret_cast<const float4*>(rowp + kTileBytes + ((c ^ sw) << 4));
+            const float2 a = conv2<MODE, ACT>(make_float2(q.x, q.y), make_float2(p.x, p.y));
+            const float2 bq = conv2<MODE, ACT>(make_float2(q.z, q.w), make_float2(p.z, p.w));
+            tc::split_hl2(a, h[4 * c4], h[4 * c4 + 1], l[4 * c4], l[4 * c4 + 1]);
+            tc::split_hl2(bq, h[4 * c4 + 2], h[4 * c4 + 3], l[4 * c4 + 2], l[4 * c4 + 3]);
+          }
         }
         if (half == 0) tc::mbar_wait(&at_empty[b], ((i >> 1) & 1) ^ 1);
         tc::tmem_st16(tmem + cAT + 64 * b + 16 * half + quarter_off, h);
@@ -463,16 +489,29 @@ __global__ void __launch_bounds__(kThreads2, 1)
       if (lane == 0) {
         tc::tma_prefetch_desc(&tm_src);
         if (GRAD) tc::tma_prefetch_desc(&tm_pre);
+        if (zpair) {
+          tc::tma_prefetch_desc(&tm_src_odd);
+          if (GRAD) tc::tma_prefetch_desc(&tm_pre_odd);
+        }
         GroupIdx gi;
         int tb = 0;
         for (int j = 0; j < n_tiles; ++j) {
           const int s = j % S, n = j / S;
           const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
           tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
-          tc::mbar_expect_tx(&full[s], L.srcs * kTileBytes);
-          unsigned char* dst = smem + L.off_ring + s * L.srcs * kTileBytes;
-          tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
-          if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+          tc::mbar_expect_tx(&full[s], L.srcs * L.tile);
+          unsigned char* dst = smem + L.off_ring + s * L.srcs * L.tile;
+          if (zpair) {  // even z rows, odd z rows (the odd map starts 2 floats early)
+            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+            tc::tma_load_4d(dst + kPairHalf, &tm_src_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+            if (GRAD) {
+              tc::tma_load_4d(dst + L.tile, &tm_pre, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+              tc::tma_load_4d(dst + L.tile + kPairHalf, &tm_pre_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+            }
+          } else {
+            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+            if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+          }
           if (++tb == L.ntb) {
             tb = 0;
             gi.next(L);
@@ -649,27 +688,36 @@ int smem_optin() {
 template <int MODE, int ACT>
 int launch2(const dfno_geom& g, const void* src, const void* pre, double scale, void* out, cudaStream_t st) {
   const int cap = smem_optin();
-  const Lay L = make_lay(g.ny, g.nz, g.nt, MODE == DFNO_SRC_GRAD ? 2 : 1, cap);
-  if (L.stages < 2) return DFNO_ERR_UNSUPPORTED;
   const int slabs = g.batch * g.c * x_local(g);
-  CUtensorMap ms, mp;
-  // TMA when the t rows start on 16-byte boundaries, cp.async otherwise
-  bool tma = g.nt % 4 == 0 && !((uintptr_t)src & 15) && !(pre && ((uintptr_t)pre & 15)) &&
+  constexpr bool GRADM = MODE == DFNO_SRC_GRAD;
+  CUtensorMap ms, mp, ms2, mp2;
+  memset(&ms2, 0, sizeof(ms2));
+  memset(&mp2, 0, sizeof(mp2));
+  const bool al16 = !((uintptr_t)src & 15) && !(pre && ((uintptr_t)pre & 15));
+  // 1) N_t % 4 == 0: one 128B-swizzled map per source; 2) N_t % 4 == 2, N_z
+  // even: even / odd z-row maps (make_slab_pair_maps); 3) otherwise cp.async
+  bool tma = g.nt % 4 == 0 && al16 &&
              make_slab_map(&ms, src, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-  if (tma && MODE == DFNO_SRC_GRAD)
-    tma = make_slab_map(&mp, pre, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-  if (!tma) {
+  if (tma && GRADM) tma = make_slab_map(&mp, pre, g.ny, g.nz, g.nt, slabs, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  bool pair = !tma && al16 && make_slab_pair_maps(&ms, &ms2, src, g.ny, g.nz, g.nt, slabs);
+  if (pair && GRADM) pair = make_slab_pair_maps(&mp, &mp2, pre, g.ny, g.nz, g.nt, slabs);
+  const Lay L = make_lay(g.ny, g.nz, g.nt, GRADM ? 2 : 1, cap, pair ? kPairTile : kTileBytes);
+  if (L.stages < 2) return DFNO_ERR_UNSUPPORTED;
+  if (!tma && !pair) {
     const uintptr_t piece = (g.nt % 2 == 0) ? 7 : 3;
     if (((uintptr_t)src & piece) || (pre && ((uintptr_t)pre & piece))) return DFNO_ERR_UNSUPPORTED;
     memset(&ms, 0, sizeof(ms));
   }
-  if (MODE != DFNO_SRC_GRAD || !tma) mp = ms;
+  if (!GRADM || (!tma && !pair)) {
+    mp = ms;
+    mp2 = ms2;
+  }
   auto kern = k_yzt_fwd_tc2<MODE, ACT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total + 1024) != cudaSuccess)
     return DFNO_ERR_UNSUPPORTED;
   const int grid = sm_count2() < slabs ? sm_count2() : slabs;
-  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, (const float*)src, (const float*)pre, tma ? 0 : 1,
-                                                (float)scale, (float2*)out, cap);
+  kern<<<grid, kThreads2, L.total + 1024, st>>>(g, ms, mp, ms2, mp2, (const float*)src, (const float*)pre,
+                                                (tma || pair) ? 0 : 1, pair ? 1 : 0, (float)scale, (float2*)out, cap);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }

@@ -38,6 +38,31 @@ inline bool make_slab_map(CUtensorMap* m, const void* base, int ny, int nz, int 
          CUDA_SUCCESS;
 }
 
+// N_t % 4 == 2 (the CO2 grid's 86) with N_z even: a row stride of N_t floats
+// is not 16-byte aligned, but two rows are.  Two 4-D maps over (t, z pair, y,
+// slab) with row stride 2 N_t: the even map starts at the tensor, the odd map
+// 2 floats before the first odd row (16-byte aligned), with inner extent
+// N_t + 2, so inner coordinate c is element c - 2 of an odd row.  Box (36, 8,
+// 8, 1), no swizzle: a 32-t block of an odd row sits 8 bytes into its 144-byte
+// line.  Out-of-range t, z and y are zero-filled by the map bounds.
+inline bool make_slab_pair_maps(CUtensorMap* even, CUtensorMap* odd, const void* base, int ny, int nz, int nt,
+                                int slabs) {
+  auto enc = tensor_map_encoder();
+  if (!enc || nt % 4 != 2 || nz % 2 != 0 || ((uintptr_t)base & 15)) return false;
+  cuuint64_t strides[3] = {(cuuint64_t)2 * nt * 4, (cuuint64_t)nz * nt * 4, (cuuint64_t)ny * nz * nt * 4};
+  cuuint32_t box[4] = {36, 8, 8, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cuuint64_t de[4] = {(cuuint64_t)nt, (cuuint64_t)(nz / 2), (cuuint64_t)ny, (cuuint64_t)slabs};
+  cuuint64_t dodd[4] = {(cuuint64_t)nt + 2, (cuuint64_t)(nz / 2), (cuuint64_t)ny, (cuuint64_t)slabs};
+  const char* ob = static_cast<const char*>(base) + (nt - 2) * 4;
+  return enc(even, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), de, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+         enc(odd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<char*>(ob), dodd, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2-D fp32 map over (point, row) of a (rows, npts) tensor, box (128, box_rows),
 // no swizzle: rows of a channel-major activation viewed as (b * c, points).
 inline bool make_rows_map(CUtensorMap* m, const void* base, long long npts, long long rows, int box_rows) {
