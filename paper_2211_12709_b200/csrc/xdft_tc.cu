@@ -82,11 +82,13 @@ __host__ __device__ inline XLay make_xlay(int nx, int xmax, int xcnt, bool red) 
 template <bool INV>
 __device__ void build_twiddles(const dfno_geom& g, const XLay& L, unsigned char* smem, int x0) {
   float4* ph = reinterpret_cast<float4*>(smem + L.off_ph);
+  // fp32 sincospif (<= 1 ulp, exact phase reduction already done) then the
+  // hi / lo split of the fp32 value: the pair carries the twiddle to ~2^-24
   for (int j = threadIdx.x; j < g.nx; j += blockDim.x) {
-    double s, c;
-    sincospi(2.0 * (double)j / g.nx, &s, &c);
-    const float ch = tc::round_tf32((float)c), sh = tc::round_tf32((float)s);
-    ph[j] = make_float4(ch, tc::round_tf32((float)(c - (double)ch)), sh, tc::round_tf32((float)(s - (double)sh)));
+    float s, c;
+    sincospif(2.0f * (float)j / (float)g.nx, &s, &c);
+    const float ch = tc::round_tf32(c), sh = tc::round_tf32(s);
+    ph[j] = make_float4(ch, tc::round_tf32(c - ch), sh, tc::round_tf32(s - sh));
   }
   __syncthreads();
   float* b = reinterpret_cast<float*>(smem + L.off_b);
