@@ -54,10 +54,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-train", action="store_true")
     p.add_argument("--sample-ranks", type=int, default=16, help="CPU sample: 1/R of the job per process")
-    p.add_argument("--config", choices=["auto", "C3", "C4rank"], default="auto",
+    p.add_argument("--config", choices=["auto", "C3", "C4rank", "C5rank"], default="auto",
                    help="auto: C2 at N = 1, C5 weak scaling under torchrun; C3: 128^3x32 on one GPU; C4rank: the "
                         "CO2 grid 262x118x64x86 as 8 thread-ranks on one GPU (every launch has a P = 8 rank's "
-                        "geometry)")
+                        "geometry); C5rank: the P = 8 weak-scaling problem as 8 thread-ranks on one GPU")
     return p.parse_args()
 
 
@@ -505,6 +505,9 @@ SINGLE_GPU_CONFIGS = {
     "C4rank": ((262, 118, 64, 86), 8, "C4 CO2 FNO 262x118x64x86 (1.98 M cells x 86 steps), width 20, 4 blocks, "
                                       "modes 8, batch 1, fwd+bwd, as 8 thread-ranks on one B200 (x slabs 33x6 + "
                                       "32x2, ky pencils of 2)"),
+    "C5rank": ((512, 64, 64, 32), 8, "C5 weak scaling at P = 8: global 512x64x64x32 (one 64x64x64x32 slab per "
+                                     "rank), width 20, 4 blocks, modes 8, batch 1, fwd+bwd, as 8 thread-ranks on one "
+                                     "B200 (ky pencils of 2, x-DFT over 512)"),
 }
 
 
