@@ -112,8 +112,9 @@ __host__ __device__ inline Lay make_lay(int ny, int nz, int nt, int srcs, int sm
   L.off_ring = o;
   const int stage = srcs * tile;
   int s = (smem_cap - o) / stage;
-  // two converter sets need an even depth: ring stage s always holds tiles of parity s & 1
-  s = s >= 4 ? 4 : (s >= 2 ? 2 : 0);
+  // up to 4 stages; an odd depth makes a stage alternate between the two
+  // converter sets, whose waits then check the stage's previous phase first
+  s = s >= 4 ? 4 : (s >= 2 ? s : 0);
   L.stages = s;
   L.tile = tile;
   L.total = o + s * stage;
@@ -171,7 +172,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
   constexpr bool GRAD = (MODE == DFNO_SRC_GRAD);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[4], empty[4], at_full[2], at_empty[2], d1_full[2], d1_empty[2];
+  // full: one barrier per (converter set, stage), so each set sees exactly
+  // one phase per tile of its own even when an odd ring depth makes a stage
+  // alternate between the sets
+  __shared__ uint64_t full[2][4], empty[4], at_full[2], at_empty[2], d1_full[2], d1_empty[2];
   __shared__ uint64_t az_full[2], az_empty[2], d2_full[2], d2_empty[2], ay_full, ay_empty, d3_full, d3_empty;
   __shared__ uint64_t by_full[2], by_empty[2];
   __shared__ uint32_t tmem_base;
@@ -217,7 +221,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
   if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
   if (tid == 0) {
     for (int s = 0; s < 4; ++s) {
-      tc::mbar_init(&full[s], use_ca ? 64 : 1);  // cp.async: one arrival per producer lane (2 warps)
+      tc::mbar_init(&full[0][s], use_ca ? 64 : 1);  // cp.async: one arrival per producer lane (2 warps)
+      tc::mbar_init(&full[1][s], use_ca ? 64 : 1);
       tc::mbar_init(&empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           }
         }
       }
-      tc::cp_async_mbar_arrive(&full[s]);
+      tc::cp_async_mbar_arrive(&full[j & 1][s]);
       if (++tb == L.ntb) {
         tb = 0;
         gi.next(L);
@@ -330,7 +335,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int sw = r & 7;
     for (int i = set; set < kSets && i < n_tiles; i += kSets) {
       const int s = i % S, n = i / S;
-      tc::mbar_wait_lazy(&full[s], n & 1, 32);
+      // this set's uses of stage s: every fill (even depth) or every other (odd)
+      tc::mbar_wait_lazy(&full[set][s], ((S & 1) ? (n >> 1) : n) & 1, 32);
       const unsigned char* ring = smem + L.off_ring + s * L.srcs * L.tile;
       const unsigned char* rowp = ring + r * 128;
       const int b = i & 1;
@@ -499,18 +505,18 @@ __global__ void __launch_bounds__(kThreads2, 1)
           const int s = j % S, n = j / S;
           const int slab = (int)blockIdx.x + gi.slab_g * (int)gridDim.x;
           tc::mbar_wait_lazy(&empty[s], (n & 1) ^ 1, 64);
-          tc::mbar_expect_tx(&full[s], L.srcs * L.tile);
+          tc::mbar_expect_tx(&full[j & 1][s], L.srcs * L.tile);
           unsigned char* dst = smem + L.off_ring + s * L.srcs * L.tile;
           if (zpair) {  // even z rows, odd z rows (the odd map starts 2 floats early)
-            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
-            tc::tma_load_4d(dst + kPairHalf, &tm_src_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[j & 1][s]);
+            tc::tma_load_4d(dst + kPairHalf, &tm_src_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[j & 1][s]);
             if (GRAD) {
-              tc::tma_load_4d(dst + L.tile, &tm_pre, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
-              tc::tma_load_4d(dst + L.tile + kPairHalf, &tm_pre_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[s]);
+              tc::tma_load_4d(dst + L.tile, &tm_pre, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[j & 1][s]);
+              tc::tma_load_4d(dst + L.tile + kPairHalf, &tm_pre_odd, tb * 32, gi.zb * 8, gi.yc * 8, slab, &full[j & 1][s]);
             }
           } else {
-            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
-            if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[s]);
+            tc::tma_load_4d(dst, &tm_src, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[j & 1][s]);
+            if (GRAD) tc::tma_load_4d(dst + kTileBytes, &tm_pre, tb * 32, gi.zb * 16, gi.yc * 8, slab, &full[j & 1][s]);
           }
           if (++tb == L.ntb) {
             tb = 0;
