@@ -131,11 +131,17 @@ constexpr int kMixBwdThreads = 256;
 //   phase 1  gp[o][v] = gout * act'(pre)            (registers + smem Gs[o][p])
 //   phase 2  a[i][v]  = f(src); gin[i] = sum_o gp[o] w[i][o]   (smem As[i][p])
 //   phase 3  gW partial (4x4 register tiles per thread, point groups)
+//
+// Channel blocks (widths above 32): the launch covers input channels
+// [i0, i0 + cin) and output channels [o0, o0 + cout) of a (cin_tot, cout_tot)
+// mixer; the input gradient of the block is written (first output block) or
+// added (gin_add), and the weight-gradient partial lands at its block of the
+// CTA's (cin_tot x cout_tot) partial.
 template <typename R, int CM, int V>
 __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
     long long npts, int nb, int cin, int cout, const R* __restrict__ gout, const R* __restrict__ pre,
     const R* __restrict__ src, int src_act, int act, const R* __restrict__ w, R* __restrict__ gin,
-    R* __restrict__ partials) {
+    R* __restrict__ partials, int cin_tot, int cout_tot, int i0, int o0, int gin_add) {
   constexpr int TP = kMixBwdThreads * V;      // points per tile
   constexpr int NB4 = CM / 4;
   constexpr int NPAIR = NB4 * NB4;
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
 
   for (int k = threadIdx.x; k < CM * CM; k += blockDim.x) {
     const int i = k / CM, o = k % CM;
-    ws[k] = (i < cin && o < cout) ? w[(long long)i * cout + o] : (R)0;
+    ws[k] = (i < cin && o < cout) ? w[(long long)(i0 + i) * cout_tot + o0 + o] : (R)0;
   }
   const int tid = threadIdx.x;
   const int pair = tid % NPAIR, grp = tid / NPAIR;
@@ -170,8 +176,8 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
     __syncthreads();  // previous tile's As / Gs consumed
     // ---- phase 1: gp = gout * act'(pre)
     R gp[CM][V];
-    const R* go = gout + bb * cout * npts + p;
-    const R* pr = pre + bb * cout * npts + p;
+    const R* go = gout + (bb * cout_tot + o0) * npts + p;
+    const R* pr = pre + (bb * cout_tot + o0) * npts + p;
 #pragma unroll
     for (int o = 0; o < CM; ++o) {
       R gv[V], pv[V];
@@ -191,8 +197,8 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
       stv<R, V>(Gs + o * TP + tid * V, gp[o]);
     }
     // ---- phase 2: a = f(src) -> As ; gin = sum_o gp w
-    const R* sp = src + bb * cin * npts + p;
-    R* gi = gin ? gin + bb * cin * npts + p : nullptr;
+    const R* sp = src + (bb * cin_tot + i0) * npts + p;
+    R* gi = gin ? gin + (bb * cin_tot + i0) * npts + p : nullptr;
     for (int i = 0; i < CM; ++i) {
       if (i >= cin) {
         R z[V];
@@ -225,11 +231,17 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
           for (int k = 0; k < V; ++k) s[k] = fma(gp[o][k], wv, s[k]);
         }
         if (full) {
+          if (gin_add) {
+            R prev[V];
+            ldv<R, V>(gi + (long long)i * npts, prev);
+#pragma unroll
+            for (int k = 0; k < V; ++k) s[k] += prev[k];
+          }
           stv<R, V>(gi + (long long)i * npts, s);
         } else {
 #pragma unroll
           for (int k = 0; k < V; ++k)
-            if (p + k < npts) gi[(long long)i * npts + k] = s[k];
+            if (p + k < npts) gi[(long long)i * npts + k] = gin_add ? gi[(long long)i * npts + k] + s[k] : s[k];
         }
       }
     }
@@ -261,14 +273,14 @@ __global__ void __launch_bounds__(kMixBwdThreads) k_mix_bwd(
       for (int b = 0; b < 4; ++b) red[grp * NPAIR * 16 + pair * 16 + a * 4 + b] = acc[a][b];
   }
   __syncthreads();
-  R* outp = partials + (long long)blockIdx.x * cin * cout;
+  R* outp = partials + (long long)blockIdx.x * cin_tot * cout_tot;
   for (int e = tid; e < NPAIR * 16; e += blockDim.x) {
     R s = (R)0;
     for (int gI = 0; gI < NGRP; ++gI) s += red[gI * NPAIR * 16 + e];
     const int pr2 = e / 16, ab = e % 16;
     const int i = (pr2 / NB4) * 4 + ab / 4;
     const int o = (pr2 % NB4) * 4 + ab % 4;
-    if (i < cin && o < cout) outp[i * cout + o] = s;
+    if (i < cin && o < cout) outp[(long long)(i0 + i) * cout_tot + o0 + o] = s;
   }
 }
 
@@ -367,7 +379,7 @@ static int mix_bwd_cm(int cin, int cout) {
   if (m <= 20) return 20;
   if (m <= 24) return 24;
   if (m <= 32) return 32;
-  return -1;
+  return 64;  // channel blocks of 32 (mix_bwd_dispatch)
 }
 
 template <typename R>
@@ -385,10 +397,14 @@ static int mix_bwd_blocks(long long npts, int nb) {
   return (int)blocks;
 }
 
+struct MixBlock {
+  int cin_tot, cout_tot, i0, o0, gin_add;
+};
+
 template <typename R, int CM, int V>
 static int launch_mix_bwd_v(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
                             const void* src, int src_act, int act, const void* w, void* gin, void* partials,
-                            cudaStream_t st) {
+                            cudaStream_t st, MixBlock blk) {
   constexpr int NB4 = CM / 4;
   constexpr int NPAIR = NB4 * NB4;
   constexpr int NGRP = (kMixBwdThreads / NPAIR) > 0 ? (kMixBwdThreads / NPAIR) : 1;
@@ -399,7 +415,8 @@ static int launch_mix_bwd_v(long long npts, int nb, int cin, int cout, const voi
     return DFNO_ERR_UNSUPPORTED;
   const int blocks = mix_bwd_blocks(npts, nb);
   kern<<<blocks, kMixBwdThreads, smem, st>>>(npts, nb, cin, cout, (const R*)gout, (const R*)pre, (const R*)src,
-                                             src_act, act, (const R*)w, (R*)gin, (R*)partials);
+                                             src_act, act, (const R*)w, (R*)gin, (R*)partials, blk.cin_tot,
+                                             blk.cout_tot, blk.i0, blk.o0, blk.gin_add);
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }
@@ -407,14 +424,16 @@ static int launch_mix_bwd_v(long long npts, int nb, int cin, int cout, const voi
 template <typename R, int CM>
 static int launch_mix_bwd(long long npts, int nb, int cin, int cout, const void* gout, const void* pre,
                           const void* src, int src_act, int act, const void* w, void* gin, void* partials,
-                          cudaStream_t st) {
+                          cudaStream_t st, MixBlock blk = MixBlock{-1, -1, 0, 0, 0}) {
+  if (blk.cin_tot < 0) blk = MixBlock{cin, cout, 0, 0, 0};
   constexpr int V = mix_bwd_v<R>();
   // vector path needs every row V-aligned
   const bool aligned = (npts % V == 0) && ((uintptr_t)gout % (V * sizeof(R)) == 0) &&
                        ((uintptr_t)pre % (V * sizeof(R)) == 0) && ((uintptr_t)src % (V * sizeof(R)) == 0) &&
                        (gin == nullptr || (uintptr_t)gin % (V * sizeof(R)) == 0);
-  if (aligned) return launch_mix_bwd_v<R, CM, V>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
-  return launch_mix_bwd_v<R, CM, 1>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
+  if (aligned)
+    return launch_mix_bwd_v<R, CM, V>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st, blk);
+  return launch_mix_bwd_v<R, CM, 1>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st, blk);
 }
 
 template <typename R>
@@ -429,8 +448,19 @@ static int mix_bwd_dispatch(long long npts, int nb, int cin, int cout, const voi
     case 20: return launch_mix_bwd<R, 20>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
     case 24: return launch_mix_bwd<R, 24>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
     case 32: return launch_mix_bwd<R, 32>(npts, nb, cin, cout, gout, pre, src, src_act, act, w, gin, partials, st);
-    default: return DFNO_ERR_UNSUPPORTED;
+    default: break;
   }
+  // wider mixers: 32 x 32 channel blocks; the input gradient of an input block
+  // is written by its first output block and accumulated by the rest (stream
+  // order), each block pair fills its part of the per-CTA weight partials
+  for (int i0 = 0; i0 < cin; i0 += 32)
+    for (int o0 = 0; o0 < cout; o0 += 32) {
+      const int ni = cin - i0 < 32 ? cin - i0 : 32, no = cout - o0 < 32 ? cout - o0 : 32;
+      const int rc = launch_mix_bwd<R, 32>(npts, nb, ni, no, gout, pre, src, src_act, act, w, gin, partials, st,
+                                           MixBlock{cin, cout, i0, o0, o0 > 0 ? 1 : 0});
+      if (rc != DFNO_OK) return rc;
+    }
+  return DFNO_OK;
 }
 
 int mix_bwd_tc(long long npts, int nb, int cin, int cout, const void* gout, const void* pre, const void* src,

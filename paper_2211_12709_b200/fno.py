@@ -608,20 +608,23 @@ def clear_plans(comm: Optional[Communicator] = None) -> None:
         comm.__dict__.pop("_dfno_plans", None)
 
 
-MAX_CHANNELS = 32  # mixer backward and fused x-spectral kernels hold a channel row in registers
+MAX_CHANNELS_F64 = 32  # the fused fp64 x-spectral kernel keeps a channel row per thread
 
 
 def check_envelope(config: FnoConfig) -> None:
     """Reject, before any kernel runs, configurations outside the kernels'
-    envelope (the reference itself accepts any width): every channel count
-    must be <= MAX_CHANNELS."""
+    envelope (the reference itself accepts any width): fp32 takes any channel
+    width (wider mixers run in 32-channel blocks); the real64 path is limited to
+    MAX_CHANNELS_F64 channels."""
+    if config.dtype != DType.REAL64:
+        return
     widths = {"in_channels": config.in_channels, "hidden_channels": config.hidden_channels,
               "out_channels": config.out_channels}
-    wide = {k: v for k, v in widths.items() if v > MAX_CHANNELS}
+    wide = {k: v for k, v in widths.items() if v > MAX_CHANNELS_F64}
     if wide:
         raise DimensionMismatchError(
-            f"channel widths {wide} exceed the B200 kernels' limit of {MAX_CHANNELS} channels "
-            f"(mixer backward and spectral contraction keep one channel row per thread)")
+            f"channel widths {wide} exceed the real64 kernels' limit of {MAX_CHANNELS_F64} channels "
+            f"(real32 takes any width)")
 
 
 def _on_device(t: DenseTensor, plan: _Plan, dtype: torch.dtype, what: str) -> torch.Tensor:

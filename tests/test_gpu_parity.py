@@ -217,3 +217,22 @@ def test_replicated_mixer_grads_bit_identical_across_ranks(pipeline):
     res = run_fwd_bwd(config, x, we, wd, blocks)[6]
     for r in res[1:]:
         assert P.bit_equal(r[2].we, res[0][2].we) and P.bit_equal(r[2].wd, res[0][2].wd)
+
+
+@pytest.mark.parametrize("cin,c,cout,ranks", [(3, 40, 36, 1), (36, 64, 5, 2)])
+def test_wide_channels_against_oracle(cin, c, cout, ranks):
+    # widths above 32 (the reference takes any width): the mixers run in
+    # 32-channel blocks, the spectral contraction over every channel
+    rng = np.random.default_rng(9)
+    meta = {"grid": [16, 12, 8, 8], "modes": [4, 4, 3, 3], "channels": c, "in_channels": cin, "out_channels": cout,
+            "blocks": 2, "activation": "gelu", "dtype": "real64"}
+    params = P.init_params(make_config(meta, 1), 9, device="cpu")
+    x = rng.standard_normal((1, cin) + tuple(meta["grid"]))
+    we, wd, blocks = params.we.numpy(), params.wd.numpy(), [w.numpy() for w in params.blocks]
+    config = make_config(meta, ranks, "real32")
+    y, gx, gwe, gwd, gws, _, _ = run_fwd_bwd(config, x, we, wd, blocks)
+    ry, cache = O.forward(x, we, wd, blocks, meta["modes"], with_cache=True)
+    rgx, rgwe, rgwd, rgws = O.backward(ry, we, wd, blocks, meta["modes"], cache)
+    assert O.rel_err(y, ry) < TOL32_Y
+    for a, b in [(gx, rgx), (gwe, rgwe), (gwd, rgwd)] + list(zip(gws, rgws)):
+        assert O.rel_err(a, b) < TOL32_G

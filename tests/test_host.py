@@ -125,13 +125,13 @@ def test_truncate_pad_adjoint_host_tensors():
 
 
 def test_channel_envelope_rejected_before_any_kernel():
-    # the mixer backward / spectral contraction keep a channel row per thread:
-    # widths above 32 are refused when the plan is built, not mid-backward
+    # real64 keeps a channel row per thread in its fused x-spectral kernel:
+    # widths above 32 are refused when the plan is built; real32 takes any width
     import paper_2211_12709_b200 as P
     from paper_2211_12709_b200 import fno as F
 
-    ok = P.FnoConfig(8, 8, 8, 4, 32, 32, 32, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real32", 1)
-    F.check_envelope(ok)
-    wide = P.FnoConfig(8, 8, 8, 4, 3, 3, 40, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real32", 1)
+    F.check_envelope(P.FnoConfig(8, 8, 8, 4, 3, 3, 64, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real32", 1))
+    F.check_envelope(P.FnoConfig(8, 8, 8, 4, 32, 32, 32, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real64", 1))
+    wide = P.FnoConfig(8, 8, 8, 4, 3, 3, 40, P.ModeSpec.of_xyzt(2, 2, 2, 2), 1, "gelu", "real64", 1)
     with pytest.raises(P.DimensionMismatchError, match="hidden_channels"):
         F.check_envelope(wide)
