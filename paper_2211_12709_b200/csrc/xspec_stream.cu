@@ -230,55 +230,56 @@ __device__ __forceinline__ void cmac2_conj_b(float4& acc, const float4& a, const
   acc.w = fmaf(a.w, b.z, acc.w); acc.w = fmaf(-a.z, b.w, acc.w);
 }
 
-__global__ void __launch_bounds__(kXT, 3) k_xmix2(const dfno_geom g, const float4* __restrict__ X,
+template <int OG>
+__global__ void __launch_bounds__(kXT) k_xmix2(const dfno_geom g, const float4* __restrict__ X,
                                                const float4* __restrict__ W, float4* __restrict__ Y) {
   const long long mloc = mloc_of(g);
-  const int C = g.c, nog = (C + kOG - 1) / kOG;
+  const int C = g.c, nog = (C + OG - 1) / OG;
   const long long cols = (long long)g.rx * mloc / 2;  // column pairs
   const long long n = (long long)nog * cols;
   for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
     const long long col = e % cols;
-    const int o0 = (int)(e / cols) * kOG;
+    const int o0 = (int)(e / cols) * OG;
     for (int bb = 0; bb < g.batch; ++bb) {
-      float4 acc[kOG];
+      float4 acc[OG];
 #pragma unroll
-      for (int j = 0; j < kOG; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < OG; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
       const float4* xp = X + ((long long)bb * C) * cols + col;
 #pragma unroll 2
       for (int i = 0; i < C; ++i) {
         const float4 xv = xp[(long long)i * cols];
         const float4* wr = W + ((long long)i * C + o0) * cols + col;
 #pragma unroll
-        for (int j = 0; j < kOG; ++j) {
+        for (int j = 0; j < OG; ++j) {
           const float4 wv = (o0 + j < C) ? __ldcs(wr + j * cols) : make_float4(0.f, 0.f, 0.f, 0.f);
           cmac2(acc[j], xv, wv);
         }
       }
       float4* yp = Y + ((long long)bb * C + o0) * cols + col;
 #pragma unroll
-      for (int j = 0; j < kOG; ++j)
+      for (int j = 0; j < OG; ++j)
         if (o0 + j < C) yp[j * cols] = acc[j];
     }
   }
 }
 
-template <int BM>
-__global__ void __launch_bounds__(kXT, 3) k_xmix_bwd2(const dfno_geom g, const float4* __restrict__ S,
+template <int BM, int OG>
+__global__ void __launch_bounds__(kXT) k_xmix_bwd2(const dfno_geom g, const float4* __restrict__ S,
                                                    const float4* __restrict__ D, const float4* __restrict__ W,
                                                    float4* __restrict__ gW, float4* __restrict__ dX) {
   const long long mloc = mloc_of(g);
-  const int C = g.c, nig = (C + kOG - 1) / kOG, B = g.batch;
+  const int C = g.c, nig = (C + OG - 1) / OG, B = g.batch;
   const long long cols = (long long)g.rx * mloc / 2;
   const long long n = (long long)nig * cols;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (long long e = (long long)blockIdx.x * kXT + threadIdx.x; e < n; e += (long long)gridDim.x * kXT) {
     const long long col = e % cols;
-    const int i0 = (int)(e / cols) * kOG;
-    float4 sv[BM][kOG], dx[BM][kOG];
+    const int i0 = (int)(e / cols) * OG;
+    float4 sv[BM][OG], dx[BM][OG];
 #pragma unroll
     for (int bb = 0; bb < BM; ++bb)
 #pragma unroll
-      for (int j = 0; j < kOG; ++j) {
+      for (int j = 0; j < OG; ++j) {
         sv[bb][j] = (bb < B && i0 + j < C) ? S[((long long)bb * C + i0 + j) * cols + col] : z4;
         dx[bb][j] = z4;
       }
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(kXT, 3) k_xmix_bwd2(const dfno_geom g, const f
 #pragma unroll
       for (int bb = 0; bb < BM; ++bb) dv[bb] = (bb < B) ? D[((long long)bb * C + o) * cols + col] : z4;
 #pragma unroll
-      for (int j = 0; j < kOG; ++j) {
+      for (int j = 0; j < OG; ++j) {
         if (i0 + j >= C) continue;
         const long long wi = ((long long)(i0 + j) * C + o) * cols + col;
         const float4 wv = __ldcs(W + wi);
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kXT, 3) k_xmix_bwd2(const dfno_geom g, const f
 #pragma unroll
     for (int bb = 0; bb < BM; ++bb)
 #pragma unroll
-      for (int j = 0; j < kOG; ++j)
+      for (int j = 0; j < OG; ++j)
         if (bb < B && i0 + j < C) dX[((long long)bb * C + i0 + j) * cols + col] = dx[bb][j];
   }
 }
@@ -584,15 +585,62 @@ int xidft_stage(const dfno_geom& g, const void* Y, float s2, void* kx_out, cudaS
   return launch_idft(g, Y, s2, kx_out, st);
 }
 
+// Channel grouping of the weight-stream contractions.  A thread owns OG
+// channels of one column pair and streams C x OG weight pairs; the grid is the
+// resident block count and the kernels stride over it, so a launch takes
+// ceil(items / resident threads) rounds.  With OG = 4 at C2 (5 x 32768 items,
+// 444 resident blocks) that is 1.44 -> 2 rounds and a third of the GPU idles in
+// the second; the pick minimises rounds x requests per item (one shared column
+// load per channel plus OG weight loads, and OG gradient stores backward).
+// Measured at C2 (ncu, profiles/r02_ab_xmix_og.txt): OG = 1 / 2 / 4 forward
+// 45.5 / 61.0 / 78.9 us, backward 80.4 / 98.1 / 159.2 us (the earlier fixed
+// OG = 4 with an oversubscribed grid: 44.6 / 115 us).
+template <typename K>
+struct OgPick {
+  int og;
+  K kern;
+  unsigned grid;
+};
+
+template <typename K>
+OgPick<K> pick_og(const K (&ks)[3], int (&occ)[3], int C, long long cols2, int reqs_per_og) {
+  static const int ogs[3] = {1, 2, 4};
+  OgPick<K> best{0, nullptr, 0};
+  double best_cost = 0;
+  for (int i = 0; i < 3; ++i) {
+    if (!occ[i]) {  // resident blocks per SM, queried once per kernel (same value from every thread)
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks[i], kXT, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      occ[i] = per_sm;
+    }
+    const int per_sm = occ[i];
+    const long long slots = (long long)per_sm * sms_x();
+    const long long items = (long long)((C + ogs[i] - 1) / ogs[i]) * cols2;
+    const long long blocks = (items + kXT - 1) / kXT;
+    const long long rounds = (items + slots * kXT - 1) / (slots * kXT);
+    const double cost = (double)rounds * C * (1 + reqs_per_og * ogs[i]);
+    if (!best.kern || cost < best_cost) {
+      best = {ogs[i], ks[i], (unsigned)(blocks < slots ? blocks : slots)};
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
 int xmix_fwd_stage(const dfno_geom& g, const void* X, const void* w, void* Y, cudaStream_t st) {
   if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
   const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
-  if (cols % 2 == 0)
-    k_xmix2<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(g, (const float4*)X,
-                                                                                    (const float4*)w, (float4*)Y);
-  else
+  if (cols % 2 == 0) {
+    using K = void (*)(const dfno_geom, const float4*, const float4*, float4*);
+    static const K ks[3] = {k_xmix2<1>, k_xmix2<2>, k_xmix2<4>};
+    static int occ[3];
+    const auto p = pick_og(ks, occ, g.c, cols / 2, 1);
+    p.kern<<<p.grid, kXT, 0, st>>>(g, (const float4*)X, (const float4*)w, (float4*)Y);
+  } else {
     k_xmix<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(g, (const float2*)X,
                                                                                 (const float2*)w, (float2*)Y);
+  }
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
 }
@@ -602,8 +650,12 @@ int xmix_bwd_stage(const dfno_geom& g, const void* spec, const void* D, const vo
   if (!stream_ok(g)) return DFNO_ERR_UNSUPPORTED;
   const long long cols = (long long)g.rx * ky_local(g) * g.rz * g.rt;
   if (cols % 2 == 0 && g.batch == 1) {
-    k_xmix_bwd2<1><<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols / 2), kXT, 0, st>>>(
-        g, (const float4*)spec, (const float4*)D, (const float4*)w, (float4*)gw, (float4*)dX);
+    using K = void (*)(const dfno_geom, const float4*, const float4*, const float4*, float4*, float4*);
+    static const K ks[3] = {k_xmix_bwd2<1, 1>, k_xmix_bwd2<1, 2>, k_xmix_bwd2<1, 4>};
+    static int occ[3];
+    const auto p = pick_og(ks, occ, g.c, cols / 2, 2);
+    p.kern<<<p.grid, kXT, 0, st>>>(g, (const float4*)spec, (const float4*)D, (const float4*)w, (float4*)gw,
+                                   (float4*)dX);
   } else {
     auto kb = g.batch == 1 ? k_xmix_bwd<1> : (g.batch == 2 ? k_xmix_bwd<2> : k_xmix_bwd<kBMax>);
     kb<<<grid_for((long long)((g.c + kOG - 1) / kOG) * cols), kXT, 0, st>>>(

@@ -12,12 +12,26 @@ def ncu(args):
     return subprocess.run(["ncu", "-i", *args], capture_output=True, text=True).stdout
 
 
+SCALE = {"ns": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "nsecond": 1.0, "byte": 1.0,
+         "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
 def raw_metrics(rep):
+    """Rows of the raw page with durations in ns and byte counts in bytes (the
+    second CSV row holds each metric's unit, which ncu picks per value)."""
     rows = list(csv.reader(io.StringIO(ncu([rep, "--page", "raw", "--csv"]))))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
     out = []
     for r in rows[2:]:
-        out.append(dict(zip(hdr, r)))
+        d = {}
+        for k, u, v in zip(hdr, units, r):
+            if u in SCALE:
+                try:
+                    v = str(float(v.replace(",", "")) * SCALE[u])
+                except ValueError:
+                    pass
+            d[k] = v
+        out.append(d)
     return out
 
 

@@ -1,5 +1,5 @@
 """Time one libdfno kernel at the C2 geometry with CUDA events (median of N).
-Usage: python tools/time_kernel.py yzt_fwd|yzt_fwd_grad|yzt_inv|xspec_fwd|xspec_bwd|mix_fwd|mix_bwd [reps]"""
+Usage: python tools/time_kernel.py yzt_fwd|yzt_fwd_grad|yzt_inv|xspec_fwd|xspec_bwd|xdft|xmix_fwd|xmix_bwd|xidft|mix_fwd|mix_bwd [reps]"""
 import ctypes
 import os
 import statistics
@@ -29,6 +29,8 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     xk = torch.randn((1, c, grid[0], 16, 16, 16), dtype=torch.complex64, device="cuda")
     w = torch.randn((c, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
     spec = torch.randn((1, c, 16, 16, 16, 16), dtype=torch.complex64, device="cuda")
+    spec2 = torch.empty_like(spec)
+    spec3 = torch.randn_like(spec)
     out = torch.empty_like(xk)
     gw = torch.empty_like(w)
     npts = grid[0] * grid[1] * grid[2] * grid[3]
@@ -50,6 +52,11 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
         "xspec_fwd": lambda: lib.dfno_xspec_fwd(gp, _lib.ptr(xk), _lib.ptr(w), _lib.ptr(spec), _lib.ptr(out), st),
         "xspec_bwd": lambda: lib.dfno_xspec_bwd(gp, _lib.ptr(xk), _lib.ptr(spec), _lib.ptr(w), _lib.ptr(gw),
                                                 _lib.ptr(out), st),
+        "xdft": lambda: lib.dfno_xdft(gp, _lib.ptr(xk), ctypes.c_double(1.0), _lib.ptr(spec), st),
+        "xmix_fwd": lambda: lib.dfno_xmix_fwd(gp, _lib.ptr(spec), _lib.ptr(w), _lib.ptr(spec2), st),
+        "xmix_bwd": lambda: lib.dfno_xmix_bwd(gp, _lib.ptr(spec), _lib.ptr(spec3), _lib.ptr(w), _lib.ptr(gw),
+                                              _lib.ptr(spec2), st),
+        "xidft": lambda: lib.dfno_xidft(gp, _lib.ptr(spec), ctypes.c_double(1.0), _lib.ptr(out), st),
         "mix_fwd": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), None, st),
         "mix_fwd_post": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 0, _lib.ptr(w), _lib.ptr(p), _lib.ptr(b),
                                                  st),
