@@ -16,10 +16,11 @@ from paper_2211_12709_b200.partition import block_starts  # noqa: E402
 def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
     lib = _lib.load()
     ret = tuple(min(16, n) for n in grid)
-    g = _lib.make_geom(batch=1, c_in=c, c=c, c_out=c, grid=grid, modes=(8, 8, 8, 8), retained=ret, nranks=1,
+    P = int(os.environ.get("TK_P", "1"))  # rank 0 of a P-way decomposition (buffers sized for P = 1)
+    g = _lib.make_geom(batch=1, c_in=c, c=c, c_out=c, grid=grid, modes=(8, 8, 8, 8), retained=ret, nranks=P,
                        rank=0, dtype=_lib.F32,
-                       act=_lib.ACT_IDENTITY if os.environ.get("TK_ACT") == "id" else _lib.ACT_GELU, x_starts=block_starts(grid[0], 1),
-                       ky_starts=block_starts(ret[1], 1))
+                       act=_lib.ACT_IDENTITY if os.environ.get("TK_ACT") == "id" else _lib.ACT_GELU, x_starts=block_starts(grid[0], P),
+                       ky_starts=block_starts(ret[1], P))
     gp = ctypes.byref(g)
     st = _lib.stream_handle()
     a = torch.randn((1, c) + grid, device="cuda")
