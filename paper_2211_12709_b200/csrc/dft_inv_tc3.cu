@@ -21,7 +21,9 @@
 //   MMA T'   per 32-t block tb: D_T[(y,kz)][t re 32 | t im 32] = A_T . [[C,-S];[S,C]]_t
 //            (TS, N=64)
 //   T epi    warps 4-7: D_T -> stash2 -> A_Z[(y 4, t)][(kz re | kz im)] (TMEM),
-//            two Z' tiles per (chunk, t block)
+//            two Z' tiles per (chunk, t block); tile h takes y_l = 2q + h in
+//            lane quarter q, i.e. the two y rows warp q already holds in D_T, so
+//            each warp transposes through its own stash rows (no CTA barrier)
 //   MMA Z'   per 64-z block: D_Z[(y,t)][z] = Re(A_Z . e^{+i kz z}) = A_Z . [C ; -S]_z
 //            (TS, N=64; two issuers by tile parity)
 //   O epi    warps 8-15 (two sets by tile parity): D_Z -> global, one 128-byte
@@ -310,13 +312,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int c = 0; c < 64; c += 4)
         *reinterpret_cast<float4*>(dst + c) = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]),
                                                           __uint_as_float(u[c + 2]), __uint_as_float(u[c + 3]));
-      tc::named_sync(2, 128);
+      __syncwarp();  // the warp transposes only its own two y rows: no cross-warp barrier
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         const int zi = 2 * i + h, ab = zi & 1;
         tc::mbar_wait(&az_empty[ab], ((zi >> 1) & 1) ^ 1);
         tc::fence_after();
-        const float* src = s2 + ((4 * h + q) * 16) * kS2 + lane;  // A_Z row (y_l = 4h + q, t = lane)
+        const float* src = s2 + ((2 * q + h) * 16) * kS2 + lane;  // A_Z row (y_l = 2q + h, t = lane)
         float hr[32], lr[32];
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::fence_before();
         tc::mbar_arrive(&az_full[ab]);
       }
-      tc::named_sync(2, 128);  // s2 consumed
+      __syncwarp();  // s2 rows consumed
     }
   } else if (warp < wIssY3) {
     // ======================= O epilogue: D_Z -> global =======================
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const int i = u / L.ntb, tb = u - i * L.ntb;
       const int si = i / L.nyc, yc = i - si * L.nyc;
       const int slab = (int)blockIdx.x + si * (int)gridDim.x;
-      const int y = 8 * yc + 4 * h + yq, t = 32 * tb + lane;
+      const int y = 8 * yc + 2 * yq + h, t = 32 * tb + lane;  // Z' tile h holds y_l = 2q + h in lane quarter q
       float* o = out + ((long long)slab * Ny + y) * plane + t;
       for (int zo = 0; zo < L.nzo; ++zo, ++v) {
         tc::mbar_wait(&dz_full[k], v & 1);

@@ -608,6 +608,9 @@ OgPick<K> pick_og(const K (&ks)[3], int (&occ)[3], int C, long long cols2, int r
   OgPick<K> best{0, nullptr, 0};
   double best_cost = 0;
   for (int i = 0; i < 3; ++i) {
+#ifdef DFNO_XMIX_OG  // A/B experiments only (tools/og_probe.sh)
+    if (ogs[i] != DFNO_XMIX_OG) continue;
+#endif
     if (!occ[i]) {  // resident blocks per SM, queried once per kernel (same value from every thread)
       int per_sm = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks[i], kXT, 0) != cudaSuccess || per_sm < 1)
