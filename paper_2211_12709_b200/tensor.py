@@ -245,8 +245,9 @@ def einsum_channel_mix(x: DenseTensor, w: DenseTensor) -> DenseTensor:
 
 def einsum_spectral(x: DenseTensor, w: DenseTensor) -> DenseTensor:
     """Per-mode contraction Y[b, co, k] = sum_c X[b, c, k] W[c, co, k]
-    (reference tensor.py:231-255).  Standalone API form on the current GPU;
-    the FNO hot path fuses this contraction into dfno_xspec_fwd."""
+    (reference tensor.py:231-255) on the current GPU: complex64 with square
+    weights runs libdfno's x-spectral contraction kernel (the hot path calls
+    it through fno.py's x-spectral stage)."""
     _check_same_dtype(x, w)
     if x.labels[0] != DimLabel.B or x.labels[1] != DimLabel.C:
         raise DimensionMismatchError(f"spectral input must be (b, c, ...), got {x}")
@@ -258,10 +259,32 @@ def einsum_spectral(x: DenseTensor, w: DenseTensor) -> DenseTensor:
         raise DimensionMismatchError(f"spectral extents disagree: {x.shape[2:]} vs {w.shape[2:]}")
     if x.shape[1] != w.shape[0]:
         raise DimensionMismatchError(f"channel extent {x.shape[1]} does not match weight input channels {w.shape[0]}")
+    import ctypes
+
     from . import _lib
 
     if not _lib.available():
         raise _lib.ExtensionMissingError("a CUDA device is required (no CPU fallback)")
     dev = torch.device("cuda", torch.cuda.current_device())
+    b, c, co = x.shape[0], x.shape[1], w.shape[1]
+    if x.dtype == DType.COMPLEX64 and c == co and b <= 4:
+        # libdfno's weight-streaming contraction (the kernel of the fused
+        # x-spectral stage, dfno_xmix_fwd): the trailing mode dims flatten to
+        # one column index, described to it as a single-rank ky range
+        cols = 1
+        for n in x.shape[2:]:
+            cols *= int(n)
+        xd = x.data.to(dev).contiguous()
+        wd = w.data.to(dev).contiguous()
+        out = torch.empty_like(xd)
+        if cols:
+            g = _lib.make_geom(batch=b, c_in=c, c=c, c_out=c, grid=(1, cols, 1, 1), modes=(1, cols, 1, 1),
+                               retained=(1, cols, 1, 1), nranks=1, rank=0, dtype=_lib.F32,
+                               act=_lib.ACT_IDENTITY, x_starts=(0, 1), ky_starts=(0, cols))
+            _lib.check(_lib.load().dfno_xmix_fwd(ctypes.byref(g), _lib.ptr(xd), _lib.ptr(wd), _lib.ptr(out),
+                                                 _lib.stream_handle()), "dfno_xmix_fwd")
+        return DenseTensor(x.labels, out)
+    # complex128 (the real64 oracle-precision path), rectangular weights or
+    # batches above the kernel's register blocking: the device einsum
     out = torch.einsum("bi...,io...->bo...", x.data.to(dev), w.data.to(dev))
     return DenseTensor(x.labels, out.contiguous())

@@ -74,3 +74,25 @@ def test_block_forward_backward_against_oracle(ranks, dtype, tol, tolg):
     assert O.rel_err(pre, want_pre) < tol
     assert O.rel_err(gin, want_gin) < tolg
     assert O.rel_err(gw, want_gw) < tolg
+
+
+@pytest.mark.parametrize("shape", [(1, 20, 16, 16, 16, 16), (2, 5, 3, 7, 2, 3), (3, 4, 4, 2, 3, 1)])
+@pytest.mark.parametrize("dtype", [torch.complex64, torch.complex128])
+def test_einsum_spectral_against_numpy(shape, dtype):
+    """einsum_spectral (reference tensor.py:231-255): complex64 runs libdfno's
+    weight-streaming contraction (even and odd flattened mode counts, batch
+    1-3), complex128 the device einsum; both against numpy in float64."""
+    rng = np.random.default_rng(7)
+    b, c = shape[:2]
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    w = rng.standard_normal((c, c) + shape[2:]) + 1j * rng.standard_normal((c, c) + shape[2:])
+    labels = (P.DimLabel.B, P.DimLabel.C, P.DimLabel.KX, P.DimLabel.KY, P.DimLabel.KZ, P.DimLabel.KT)
+    wl = (P.DimLabel.C, P.DimLabel.CO) + labels[2:]
+    xt = P.DenseTensor(labels, torch.tensor(x, dtype=dtype, device="cuda"))
+    wt = P.DenseTensor(wl, torch.tensor(w, dtype=dtype, device="cuda"))
+    got = P.einsum_spectral(xt, wt).data.cpu().numpy()
+    xr = torch.tensor(x, dtype=dtype).to(torch.complex128).numpy()
+    wr = torch.tensor(w, dtype=dtype).to(torch.complex128).numpy()
+    want = np.einsum("bi...,io...->bo...", xr, wr)
+    tol = 1e-6 if dtype == torch.complex64 else 1e-13
+    assert np.abs(got - want).max() / np.abs(want).max() < tol
