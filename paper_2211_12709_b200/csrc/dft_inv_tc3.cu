@@ -20,10 +20,11 @@
 //   front    D_Y -> stash1 -> A_T[(y 8, kz)][(kt re | kt im)] (TMEM) per 8-y chunk
 //   MMA T'   per 32-t block tb: D_T[(y,kz)][t re 32 | t im 32] = A_T . [[C,-S];[S,C]]_t
 //            (TS, N=64)
-//   T epi    warps 4-7: D_T -> stash2 -> A_Z[(y 4, t)][(kz re | kz im)] (TMEM),
-//            two Z' tiles per (chunk, t block); tile h takes y_l = 2q + h in
-//            lane quarter q, i.e. the two y rows warp q already holds in D_T, so
-//            each warp transposes through its own stash rows (no CTA barrier)
+//   T epi    warps 4-7 and 22-25 (set h = Z' tile h): D_T -> stash2 ->
+//            A_Z[(y 4, t)][(kz re | kz im)] (TMEM), two Z' tiles per (chunk,
+//            t block); tile h takes y_l = 2q + h in lane quarter q, rows warp q
+//            of set h already holds in D_T, so each warp transposes through its
+//            own stash rows (no CTA barrier)
 //   MMA Z'   per 64-z block: D_Z[(y,t)][z] = Re(A_Z . e^{+i kz z}) = A_Z . [C ; -S]_z
 //            (TS, N=64; two issuers by tile parity)
 //   O epi    warps 8-15 (two sets by tile parity): D_Z -> global, one 128-byte
@@ -48,7 +49,8 @@ constexpr int wTepi3 = 4;    // warps 4-7
 constexpr int wOepi3 = 8;    // warps 8-15, set = (warp - 8) / 4
 constexpr int wIssY3 = 16, wIssT3 = 17, wIssZ3 = 18;  // Z': 18, 19
 constexpr int wLoad3 = 20, wTw3 = 21;
-constexpr int kWarps3 = 22;
+constexpr int wTepi3b = 22;  // warps 22-25: the second T-epilogue set (Z' tiles h = 1)
+constexpr int kWarps3 = 26;
 constexpr int kThreads3 = kWarps3 * 32;
 constexpr int kAYPlane3 = 16 * 1024;          // 128 rows x K 32 fp32
 constexpr int kBYPlane3 = 4 * 1024;           // one pass: 32 rows (re | im, y 16) x K 32
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&dt_full[b], 1);
-      tc::mbar_init(&dt_empty[b], 128);
+      tc::mbar_init(&dt_empty[b], 256);  // both T-epilogue sets read every D_T
       tc::mbar_init(&az_full[b], 128);
       tc::mbar_init(&az_empty[b], 1);
       tc::mbar_init(&dz_full[b], 1);
@@ -288,51 +290,55 @@ __global__ void __launch_bounds__(kThreads3, 1)
         }
       }
     }
-  } else if (warp < wOepi3) {
-    // ======================= T epilogue: D_T -> A_Z (two Z' tiles per unit) =======================
-    const int q = warp - wTepi3;
-    float* s2 = reinterpret_cast<float*>(smem + L.off_s2);  // [y 8][kz 16][c 64 (t re | t im)], pitch kS2
-    const int yl = 2 * q + (lane >> 4), kz = lane & 15;      // D_T row
+  } else if (warp < wOepi3 || warp >= wTepi3b) {
+    // ======================= T epilogue: D_T -> A_Z, set h builds Z' tile h =======================
+    // Set h (warps 4-7: h = 0, warps 22-25: h = 1) owns A_Z buffer h: its warp
+    // in lane quarter q takes the D_T rows y_l = 2q + h (lanes 16h..16h+15 of
+    // the quarter), transposes them through its own stash rows and writes A_Z
+    // row (y_l = 2q + h, t = lane).  One producer and one consumer (Z' issuer h)
+    // per A_Z buffer; both sets read every D_T.
+    const int h = warp >= wTepi3b ? 1 : 0, q = warp & 3;
+    float* s2 = reinterpret_cast<float*>(smem + L.off_s2) + (4 * h + q) * 16 * kS2;  // [kz 16][c 64], pitch kS2
+    const int kz = lane & 15;
+    const bool mine = (lane >> 4) == h;
     for (int i = 0; i < n_units; ++i) {
       const int b = i & 1;
       tc::mbar_wait(&dt_full[b], (i >> 1) & 1);
       tc::fence_after();
-      uint32_t u[64];
-      {
-        uint32_t (&u0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&u[0]);
-        uint32_t (&u1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&u[32]);
-        tc::tmem_ld32_nowait(tmem + jDT + 64 * b + qoff, u0);
-        tc::tmem_ld32_nowait(tmem + jDT + 64 * b + 32 + qoff, u1);
-      }
-      tc::tmem_ld_wait();
-      tc::fence_before();
-      tc::mbar_arrive(&dt_empty[b]);
-      float* dst = s2 + (yl * 16 + kz) * kS2;
+      float* dst = s2 + kz * kS2;
 #pragma unroll
-      for (int c = 0; c < 64; c += 4)
-        *reinterpret_cast<float4*>(dst + c) = make_float4(__uint_as_float(u[c]), __uint_as_float(u[c + 1]),
-                                                          __uint_as_float(u[c + 2]), __uint_as_float(u[c + 3]));
-      __syncwarp();  // the warp transposes only its own two y rows: no cross-warp barrier
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int zi = 2 * i + h, ab = zi & 1;
-        tc::mbar_wait(&az_empty[ab], ((zi >> 1) & 1) ^ 1);
-        tc::fence_after();
-        const float* src = s2 + ((2 * q + h) * 16) * kS2 + lane;  // A_Z row (y_l = 2q + h, t = lane)
-        float hr[32], lr[32];
-#pragma unroll
-        for (int k = 0; k < 16; k += 2) {
-          tc::split_hl2(make_float2(src[k * kS2], src[(k + 1) * kS2]), hr[k], hr[k + 1], lr[k], lr[k + 1]);  // kz re
-          tc::split_hl2(make_float2(src[k * kS2 + 32], src[(k + 1) * kS2 + 32]), hr[16 + k], hr[17 + k], lr[16 + k],
-                        lr[17 + k]);  // kz im
+      for (int part = 0; part < 2; ++part) {  // t re | t im
+        uint32_t u[32];
+        tc::tmem_ld32_nowait(tmem + jDT + 64 * b + 32 * part + qoff, u);
+        tc::tmem_ld_wait();
+        if (part == 1) {
+          tc::fence_before();
+          tc::mbar_arrive(&dt_empty[b]);
         }
-        tc::tmem_st32(tmem + jAZ + 64 * ab + qoff, hr);
-        tc::tmem_st32(tmem + jAZ + 64 * ab + 32 + qoff, lr);
-        tc::tmem_st_wait();
-        tc::fence_before();
-        tc::mbar_arrive(&az_full[ab]);
+        if (mine) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 4)
+            *reinterpret_cast<float4*>(dst + 32 * part + c) = make_float4(
+                __uint_as_float(u[c]), __uint_as_float(u[c + 1]), __uint_as_float(u[c + 2]), __uint_as_float(u[c + 3]));
+        }
       }
-      __syncwarp();  // s2 rows consumed
+      __syncwarp();
+      tc::mbar_wait(&az_empty[h], (i & 1) ^ 1);
+      tc::fence_after();
+      const float* src = s2 + lane;  // A_Z row (y_l = 2q + h, t = lane)
+      float hr[32], lr[32];
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        tc::split_hl2(make_float2(src[k * kS2], src[(k + 1) * kS2]), hr[k], hr[k + 1], lr[k], lr[k + 1]);  // kz re
+        tc::split_hl2(make_float2(src[k * kS2 + 32], src[(k + 1) * kS2 + 32]), hr[16 + k], hr[17 + k], lr[16 + k],
+                      lr[17 + k]);  // kz im
+      }
+      tc::tmem_st32(tmem + jAZ + 64 * h + qoff, hr);
+      tc::tmem_st32(tmem + jAZ + 64 * h + 32 + qoff, lr);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(&az_full[h]);
+      __syncwarp();  // stash rows consumed
     }
   } else if (warp < wIssY3) {
     // ======================= O epilogue: D_Z -> global =======================
@@ -349,34 +355,34 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int zo = 0; zo < L.nzo; ++zo, ++v) {
         tc::mbar_wait(&dz_full[k], v & 1);
         tc::fence_after();
-        uint32_t w[64];
-        {
-          uint32_t (&u0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&w[0]);
-          uint32_t (&u1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&w[32]);
-          tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + qoff, u0);
-          tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + 32 + qoff, u1);
-        }
-        tc::tmem_ld_wait();
-        tc::fence_before();
-        tc::mbar_arrive(&dz_empty[k]);
-        if (FAST && Nz == 64) {
-          if (y < Ny) {
 #pragma unroll
-            for (int z = 0; z < 64; ++z) __stcs(o + z * 32, __uint_as_float(w[z]));
+        for (int half = 0; half < 2; ++half) {  // z 0-31, z 32-63 of the block (32 live registers)
+          uint32_t w[32];
+          tc::tmem_ld32_nowait(tmem + jDZ + 64 * k + 32 * half + qoff, w);
+          tc::tmem_ld_wait();
+          if (half == 1) {
+            tc::fence_before();
+            tc::mbar_arrive(&dz_empty[k]);
           }
-        } else if (NT > 0 && ZFULL) {
-          if (y < Ny && t < Nt) {
-            float* oz = o + (long long)(64 * zo) * Nt;
+          if (FAST && Nz == 64) {
+            if (y < Ny) {
 #pragma unroll
-            for (int z = 0; z < 64; ++z) __stcs(oz + z * Nt, __uint_as_float(w[z]));
-          }
-        } else if (y < Ny && t < Nt) {
-          float* oz = o + (long long)(64 * zo) * Nt;
-          const int zn = min(64, Nz - 64 * zo);
+              for (int z = 0; z < 32; ++z) __stcs(o + (32 * half + z) * 32, __uint_as_float(w[z]));
+            }
+          } else if (NT > 0 && ZFULL) {
+            if (y < Ny && t < Nt) {
+              float* oz = o + (long long)(64 * zo + 32 * half) * Nt;
 #pragma unroll
-          for (int z = 0; z < 64; ++z) {
-            if (z < zn) __stcs(oz, __uint_as_float(w[z]));
-            oz += Nt;
+              for (int z = 0; z < 32; ++z) __stcs(oz + z * Nt, __uint_as_float(w[z]));
+            }
+          } else if (y < Ny && t < Nt) {
+            float* oz = o + (long long)(64 * zo + 32 * half) * Nt;
+            const int zn = min(64, Nz - 64 * zo) - 32 * half;
+#pragma unroll
+            for (int z = 0; z < 32; ++z) {
+              if (z < zn) __stcs(oz, __uint_as_float(w[z]));
+              oz += Nt;
+            }
           }
         }
       }
