@@ -12,8 +12,8 @@
 //   loader   warp 20: V (16 contiguous (kz, kt) blocks per slab) -> shared, bulk
 //            copies one slab ahead
 //   twiddle  warp 21: the Y' operand of each 16-y pass (hi / lo planes) from a
-//            phase table into a two-slot ring (one slot when shared memory is
-//            short), so no N_y-sized table is resident
+//            phase table: all passes built once when shared memory holds them
+//            (N_y <= 64), else into a two-slot ring (one slot when short)
 //   front    warps 0-3: V -> A_Y (shared), rows (kz, kt) [2 tiles], K = (ky re | ky im)
 //   MMA Y'   D_Y[(kz,kt)][y re 16 | y im 16] = A_Y . [[C,-S];[S,C]]_y  (SS, N=32,
 //            16 y per pass)
@@ -392,14 +392,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
     if (lane == 0) {
       const uint32_t id = tc::idesc_tf32(128, 32);
       const uint32_t say = tc::smem_u32(ay);
+      const bool resident = L.nby >= L.npass;  // every pass's operand built once, before the first slab
       int pass_i = 0;
       for (int si = 0; si < my_slabs; ++si) {
         tc::mbar_wait_lazy(&ay_full, si & 1, 64);
         for (int p = 0; p < L.npass; ++p, ++pass_i) {
-          const int bs = pass_i % L.nby;
+          const int bs = resident ? p : pass_i % L.nby;
           const uint32_t sby = tc::smem_u32(by + bs * 2 * kBYPlane3);
           tc::mbar_wait(&dy_empty, (pass_i & 1) ^ 1);
-          tc::mbar_wait(&by_full[bs], (pass_i / L.nby) & 1);
+          if (!resident) tc::mbar_wait(&by_full[bs], (pass_i / L.nby) & 1);
+          else if (pass_i == 0) tc::mbar_wait(&by_full[0], 0);
           tc::fence_after();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
               tc::mma_tf32(d, tc::desc(ah0 + kb, 128, 1024), tc::desc(sby + kb, 128, 1024), id, 1u);
             }
           }
-          tc::commit(&by_empty[bs]);
+          if (!resident) tc::commit(&by_empty[bs]);
           tc::commit(&dy_full);
         }
         tc::commit(&ay_empty);
@@ -471,27 +473,36 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const int ky = lane & 15, y8 = 8 * (lane >> 4);
     const bool ky_ok = ky < g.ry;
     const int f = mode_freq(ky, Ny, g.my);
-    int pass_i = 0;
-    for (int si = 0; si < my_slabs; ++si) {
-      for (int p = 0; p < L.npass; ++p, ++pass_i) {
-        const int bs = pass_i % L.nby;
-        float* hi = reinterpret_cast<float*>(by + bs * 2 * kBYPlane3);
-        float* lo = hi + kBYPlane3 / 4;
-        tc::mbar_wait_lazy(&by_empty[bs], ((pass_i / L.nby) & 1) ^ 1, 64);
+    auto build = [&](int p, int bs) {
+      float* hi = reinterpret_cast<float*>(by + bs * 2 * kBYPlane3);
+      float* lo = hi + kBYPlane3 / 4;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int yl = y8 + j, y = 16 * p + yl;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ky_ok && y < Ny) v = ph[(f * y) % Ny];
-          const int o_rr = kmaj3(yl, ky) / 4, o_ri = kmaj3(yl, 16 + ky) / 4;
-          const int o_ir = kmaj3(16 + yl, ky) / 4, o_ii = kmaj3(16 + yl, 16 + ky) / 4;
-          hi[o_rr] = v.x; lo[o_rr] = v.y;
-          hi[o_ri] = -v.z; lo[o_ri] = -v.w;
-          hi[o_ir] = v.z; lo[o_ir] = v.w;
-          hi[o_ii] = v.x; lo[o_ii] = v.y;
+      for (int j = 0; j < 8; ++j) {
+        const int yl = y8 + j, y = 16 * p + yl;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ky_ok && y < Ny) v = ph[(f * y) % Ny];
+        const int o_rr = kmaj3(yl, ky) / 4, o_ri = kmaj3(yl, 16 + ky) / 4;
+        const int o_ir = kmaj3(16 + yl, ky) / 4, o_ii = kmaj3(16 + yl, 16 + ky) / 4;
+        hi[o_rr] = v.x; lo[o_rr] = v.y;
+        hi[o_ri] = -v.z; lo[o_ri] = -v.w;
+        hi[o_ir] = v.z; lo[o_ir] = v.w;
+        hi[o_ii] = v.x; lo[o_ii] = v.y;
+      }
+    };
+    if (L.nby >= L.npass) {  // resident (N_y <= 64 leaves room): the passes are the same for every slab
+      for (int p = 0; p < L.npass; ++p) build(p, p);
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&by_full[0]);
+    } else {
+      int pass_i = 0;
+      for (int si = 0; si < my_slabs; ++si) {
+        for (int p = 0; p < L.npass; ++p, ++pass_i) {
+          const int bs = pass_i % L.nby;
+          tc::mbar_wait_lazy(&by_empty[bs], ((pass_i / L.nby) & 1) ^ 1, 64);
+          build(p, bs);
+          tc::fence_proxy_async();
+          tc::mbar_arrive(&by_full[bs]);
         }
-        tc::fence_proxy_async();
-        tc::mbar_arrive(&by_full[bs]);
       }
     }
   } else {
@@ -574,7 +585,8 @@ extern "C" int dfno_debug_wait_prof_inv(unsigned long long* host) {
 int yzt_inv_tc3(const dfno_geom& g, const void* in, double scale, void* out, cudaStream_t st) {
   if (g.dtype != DFNO_F32 || g.ry > 16 || g.rz > 16 || g.rt > 16) return DFNO_ERR_UNSUPPORTED;
   if ((g.rz * g.rt) % 2 != 0 || ((uintptr_t)in & 15)) return DFNO_ERR_UNSUPPORTED;  // 16-byte bulk copies
-  Lay3 L = make_lay3(g.ny, g.nz, g.nt, 2);
+  Lay3 L = make_lay3(g.ny, g.nz, g.nt, (g.ny + 15) / 16);  // every Y' pass resident
+  if (L.total > smem_cap_3()) L = make_lay3(g.ny, g.nz, g.nt, 2);
   if (L.total > smem_cap_3()) L = make_lay3(g.ny, g.nz, g.nt, 1);
   if (L.total > smem_cap_3()) return DFNO_ERR_UNSUPPORTED;
   const bool zfull = g.nz % 64 == 0;
