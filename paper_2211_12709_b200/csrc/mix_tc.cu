@@ -12,7 +12,7 @@
 //        stored coalesced.
 //   GEMM2 (weight grad)  D2[r][c] += sum_p A2[r][p] B2[c][p]
 //        rows r: a_hi(i) at r = i, a_lo(i) at r = 32 + i; columns c: gp_hi(o)
-//        at c = o, gp_lo(o) at c = 32 + o, so ONE M=128 N=64 K=8 MMA per 8
+//        at c = o, gp_lo(o) at c = 32 + o, so ONE M=64 N=64 K=8 MMA per 8
 //        points yields all four hi/lo cross products.  D2 accumulates kMbFlush
 //        tiles in TMEM, then warps 0-1 fold its quadrants into a per-CTA
 //        accumulator (TMEM columns 192..223, round-to-nearest fp32 adds in
@@ -22,8 +22,9 @@
 //        cost 7.5e-5 relative on the weight gradient against a random upstream
 //        gradient (tools/precision_probe.py).  The folded sums become this CTA's
 //        partial (reduced in fixed order by k_reduce_partials8: deterministic,
-//        d/training.py:77-82).  Rows 64..127 of the A2 operand alias B2 (their
-//        D2 rows are never read).
+//        d/training.py:77-82).  M = 64 reads only the 64 A2 rows
+//        that exist (an M = 128 MMA would stream 2 KB more shared memory per
+//        MMA; 743 -> 726 us at C2 in the sigma-on-source mode).
 //
 // Shared-memory operands are SWIZZLE_NONE K-major with a padded LBO of 144 B
 // so the one-point-per-thread scalar stores are bank-conflict free.  The MMAs
@@ -121,10 +122,12 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   };
 
   // fold D2 (rows 0..63: a_hi(i), a_lo(i); columns gp_hi(o) | gp_lo(o)) into
-  // ACC[row][o] (TMEM); warps 0-1, row = thread
+  // ACC[row][o] (TMEM).  GEMM2 is an M = 64 MMA: row r sits in TMEM lane
+  // 32 (r / 16) + r % 16 (tools/probes/mma_m64_probe.cu), so every warp folds
+  // the 16 rows in the first half of its lane quarter (row = 16 warp + lane)
   bool acc_live = false;
   auto fold_d2 = [&]() {
-    if (warp < 2) {
+    {
       uint32_t r0[32], r1[32];
       float v[32];
       tc::tmem_ld32_nowait(d2 + lane_off, r0);
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
     }
     if (tid == 32) {  // second issuing warp: the weight-gradient GEMM overlaps GEMM1's issue
       tc::fence_after();
-      const uint32_t id2 = tc::idesc_tf32(128, 64);
+      const uint32_t id2 = tc::idesc_tf32(64, 64);  // only rows a_hi(i), a_lo(i) (0..63) of A2 exist
       const uint32_t sa2 = tc::smem_u32(a2), sb2 = tc::smem_u32(b2);
 #pragma unroll 4
       for (int s = 0; s < kMbThreads / 8; ++s)
@@ -283,13 +286,15 @@ __global__ void __launch_bounds__(kMbThreads, 2) k_mix_bwd_tc(long long npts, in
   // ---- weight-gradient partial: a_hi and a_lo rows of ACC -> shared -> partial
   __syncthreads();  // every thread is past its last operand write
   float* st = reinterpret_cast<float*>(smem);  // [64][33], aliases A2 (all MMAs done)
-  if (it > 0 && warp < 2) {
+  if (it > 0) {
     uint32_t r0[32];
     tc::tmem_ld32_nowait(dacc + lane_off, r0);
     tc::tmem_ld_wait();
-    const int row = 32 * warp + lane;
+    const int row = 16 * warp + lane;  // M = 64 accumulator rows (see fold_d2)
+    if (lane < 16) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) st[row * 33 + c] = __uint_as_float(r0[c]);
+      for (int c = 0; c < 32; ++c) st[row * 33 + c] = __uint_as_float(r0[c]);
+    }
   }
   __syncthreads();
   float* outp = partials + (long long)blockIdx.x * cin * cout;
