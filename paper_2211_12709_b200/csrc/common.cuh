@@ -174,30 +174,12 @@ __device__ __forceinline__ float2 f2add(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
 
-// phi_fast on a pair (same polynomial, same MUFU approximations, so the
-// results are bit-identical to two phi_fast calls up to FMA contraction of
-// the unpacked form, which uses the same fused operations).
-__device__ __forceinline__ float2 phi_fast2(float2 h, float2& e) {
-  const float2 x = f2mul(make_float2(fabsf(h.x), fabsf(h.y)), f2s(0.70710678118654752f));
-  const float2 d = f2fma(f2s(0.3275911f), x, f2s(1.0f));
-  const float2 t = make_float2(rcp_approx(d.x), rcp_approx(d.y));
-  float2 p = f2fma(f2s(0.5307027145f), t, f2s(-0.7265760135f));
-  p = f2fma(p, t, f2s(0.7107068705f));
-  p = f2fma(p, t, f2s(-0.142248368f));
-  p = f2fma(p, t, f2s(0.127414796f));
-  p = f2mul(p, t);
-  const float2 a = f2mul(h, f2mul(h, f2s(-0.72134752044448170f)));
-  e = make_float2(ex2_approx(a.x), ex2_approx(a.y));
-  const float2 q = f2mul(p, e);
-  const float2 r = f2fma(q, f2s(-1.0f), f2s(0.5f));  // 0.5 - q, exact
-  return f2add(f2s(0.5f), make_float2(copysignf(r.x, h.x), copysignf(r.y, h.y)));
-}
-
-// GELU on a pair without forming Phi: h Phi(h) = relu(h) - |h| q with
-// q = 0.5 erfc(|h| / sqrt 2) = p(t) e^{-h^2 / 2} (the same A&S 7.1.26
-// polynomial as phi_fast2, t = 1 / (1 + 0.3275911 |h| / sqrt 2) with the two
-// constants folded).  Three instructions per pair fewer than h * Phi(h) (no
-// sign copy, no 0.5 + (0.5 - q) round trip); same erf approximation.
+// GELU on pairs without forming Phi: h Phi(h) = relu(h) - |h| q with
+// q = 0.5 erfc(|h| / sqrt 2) = p(t) e^{-h^2 / 2} (the A&S 7.1.26 polynomial
+// of phi_fast, t = 1 / (1 + 0.3275911 |h| / sqrt 2) with the two constants
+// folded), and GELU' = Phi + h phi with Phi = 1 - q or q by the sign of h.
+// Fewer instructions per pair than forming Phi = 0.5 + sign(h)(0.5 - q) (no
+// sign copy, no 0.5 round trip); same erf approximation.
 __device__ __forceinline__ void gelu_q2(float2 h, float2& nah, float2& q, float2& e) {
   nah = make_float2(-fabsf(h.x), -fabsf(h.y));
   const float2 d = f2fma(f2s(-0.23164188827f), nah, f2s(1.0f));
@@ -232,8 +214,11 @@ __device__ __forceinline__ float2 act_apply2(float2 h) {
 template <int ACT>
 __device__ __forceinline__ float2 act_deriv2(float2 h) {
   if constexpr (ACT == DFNO_ACT_GELU) {
-    float2 e;
-    const float2 c = phi_fast2(h, e);
+    // GELU' = Phi(h) + h phi(h), Phi = 1 - q or q by the sign of h (the same
+    // evaluation as act_both2's derivative)
+    float2 nah, q, e;
+    gelu_q2(h, nah, q, e);
+    const float2 c = make_float2(h.x > 0.f ? 1.f - q.x : q.x, h.y > 0.f ? 1.f - q.y : q.y);
     return f2fma(f2mul(h, f2s(0.3989422804014327f)), e, c);
   } else if constexpr (ACT == DFNO_ACT_RELU) {
     return make_float2(h.x > 0.f ? 1.f : 0.f, h.y > 0.f ? 1.f : 0.f);
