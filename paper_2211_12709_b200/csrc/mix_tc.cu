@@ -587,12 +587,14 @@ __global__ void __launch_bounds__(kMbThreads + 32, 4)
       const float* row = reinterpret_cast<const float*>(ring + s * stage_bytes) + tid;
       float h[32], l[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (i < CM && (EXACT || i < cin)) {
-          const float v = row[i * kMbThreads];
-          tc::split_hl(src_act ? act_apply<float>(ACT, v) : v, h[i], l[i]);
+      for (int i = 0; i < 32; i += 2) {
+        if (i < CM) {  // channel pairs (CM is even); act(0) = 0 keeps the padding zero
+          float2 v = make_float2((EXACT || i < cin) ? row[i * kMbThreads] : 0.f,
+                                 (EXACT || i + 1 < cin) ? row[(i + 1) * kMbThreads] : 0.f);
+          if (src_act) v = act_apply2<ACT>(v);
+          tc::split_hl2(v, h[i], h[i + 1], l[i], l[i + 1]);
         } else {
-          h[i] = l[i] = 0.f;
+          h[i] = l[i] = h[i + 1] = l[i + 1] = 0.f;
         }
       }
       tc::mbar_arrive(&empty[s]);

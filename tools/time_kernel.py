@@ -61,6 +61,9 @@ def main(which, reps=20, grid=(64, 64, 64, 32), c=20):
         "mix_fwd": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), None, st),
         "mix_fwd_post": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 0, _lib.ptr(w), _lib.ptr(p), _lib.ptr(b),
                                                  st),
+        "mix_fwd_enc": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 0, _lib.ptr(w), _lib.ptr(p), None, st),
+        "mix_fwd_dec": lambda: lib.dfno_mix_fwd(gp, npts, c, c, _lib.ptr(a), 1, _lib.ptr(w), _lib.ptr(p), _lib.ptr(b),
+                                                st),
         "mix_bwd_raw": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(s3), 0, _lib.ptr(w),
                                                 _lib.ptr(b), _lib.ptr(parts), st),
         "mix_bwd": lambda: lib.dfno_mix_bwd(gp, npts, c, c, _lib.ptr(a), _lib.ptr(p), _lib.ptr(s3), 1, _lib.ptr(w),
