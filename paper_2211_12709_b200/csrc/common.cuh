@@ -95,26 +95,31 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
-__device__ __forceinline__ float phi_fast(float h, float& e) {
-  const float x = fabsf(h) * 0.70710678118654752f;
-  const float t = rcp_approx(fmaf(0.3275911f, x, 1.0f));
-  // 0.5 * (a1 t + ... + a5 t^5), coefficients pre-halved
+// fp32 GELU pieces: q = 0.5 erfc(|h| / sqrt 2) = p(t) e^{-h^2 / 2} with
+// t = 1 / (1 + 0.3275911 |h| / sqrt 2) (A&S 7.1.26 erf, |error| <= 1.5e-7,
+// coefficients pre-halved, MUFU rcp / ex2), e = e^{-h^2 / 2}.  Then
+// GELU = h Phi(h) = relu(h) - |h| q and GELU' = Phi + h phi with Phi = 1 - q
+// or q by the sign of h -- the same operations as the packed pair form below,
+// so scalar and pair kernels agree bit for bit.
+__device__ __forceinline__ float gelu_q(float h, float& nah, float& e) {
+  nah = -fabsf(h);
+  const float t = rcp_approx(fmaf(-0.23164188827f, nah, 1.0f));
   float p = fmaf(0.5307027145f, t, -0.7265760135f);
   p = fmaf(p, t, 0.7107068705f);
   p = fmaf(p, t, -0.142248368f);
   p = fmaf(p, t, 0.127414796f);
   p *= t;
   e = ex2_approx(h * (h * -0.72134752044448170f));  // e^{-h^2/2} = 2^{-h^2 log2(e) / 2}
-  const float q = p * e;                             // 0.5 (1 - erf(|x|))
-  return 0.5f + copysignf(0.5f - q, h);
+  return p * e;
 }
 
 template <typename R>
 __device__ __forceinline__ R act_apply(int act, R h) {
   if (act == DFNO_ACT_GELU) {
     if constexpr (sizeof(R) == 4) {
-      float e;
-      return h * phi_fast(h, e);
+      float nah, e;
+      const float q = gelu_q(h, nah, e);
+      return fmaf(nah, q, fmaxf(h, 0.f));
     } else {
       const R inv_sqrt2 = (R)0.70710678118654752440;
       return (R)0.5 * h * ((R)1 + erf_r(h * inv_sqrt2));
@@ -128,9 +133,9 @@ template <typename R>
 __device__ __forceinline__ R act_deriv(int act, R h) {
   if (act == DFNO_ACT_GELU) {
     if constexpr (sizeof(R) == 4) {
-      float e;
-      const float c = phi_fast(h, e);
-      return fmaf(h * 0.3989422804014327f, e, c);
+      float nah, e;
+      const float q = gelu_q(h, nah, e);
+      return fmaf(h * 0.3989422804014327f, e, h > 0.f ? 1.f - q : q);
     } else {
       const R inv_sqrt2 = (R)0.70710678118654752440;
       const R inv_sqrt2pi = (R)0.39894228040143267794;
@@ -176,7 +181,7 @@ __device__ __forceinline__ float2 f2s(float v) { return make_float2(v, v); }
 
 // GELU on pairs without forming Phi: h Phi(h) = relu(h) - |h| q with
 // q = 0.5 erfc(|h| / sqrt 2) = p(t) e^{-h^2 / 2} (the A&S 7.1.26 polynomial
-// of phi_fast, t = 1 / (1 + 0.3275911 |h| / sqrt 2) with the two constants
+// of gelu_q, t = 1 / (1 + 0.3275911 |h| / sqrt 2) with the two constants
 // folded), and GELU' = Phi + h phi with Phi = 1 - q or q by the sign of h.
 // Fewer instructions per pair than forming Phi = 0.5 + sign(h)(0.5 - q) (no
 // sign copy, no 0.5 round trip); same erf approximation.
