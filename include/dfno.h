@@ -224,6 +224,11 @@ int dfno_mse_grad(const dfno_geom* g, int64_t n, const void* pred, const void* t
 int dfno_adam(const dfno_geom* g, int64_t n, void* param, const void* grad, void* m,
               void* v, double lr, double beta1, double beta2, double eps, int step,
               void* stream);
+/* Same update written to param_out (param untouched; the reference returns
+ * new parameter arrays, d/training.py:52-74, so no copy pass is needed). */
+int dfno_adam_out(const dfno_geom* g, int64_t n, const void* param, void* param_out,
+                  const void* grad, void* m, void* v, double lr, double beta1, double beta2,
+                  double eps, int step, void* stream);
 
 #ifdef __cplusplus
 }

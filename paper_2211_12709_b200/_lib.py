@@ -47,7 +47,7 @@ EXPORTS = (
     "dfno_dft_yzt_fwd", "dfno_dft_yzt_inv", "dfno_xspec_fwd", "dfno_xspec_bwd",
     "dfno_xspec_workspace", "dfno_xspec_fwd_ws", "dfno_xspec_bwd_ws",
     "dfno_xdft", "dfno_xmix_fwd", "dfno_xmix_bwd", "dfno_xidft",
-    "dfno_mse_partials", "dfno_mse_grad", "dfno_adam",
+    "dfno_mse_partials", "dfno_mse_grad", "dfno_adam", "dfno_adam_out",
 )
 
 
@@ -101,6 +101,7 @@ def load(path: Path = LIB_PATH) -> ctypes.CDLL:
         "dfno_mse_partials": ([i64, ctypes.POINTER(i32)], i32),
         "dfno_mse_grad": ([gp, i64, vp, vp, dbl, vp, vp, vp, vp], i32),
         "dfno_adam": ([gp, i64, vp, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp], i32),
+        "dfno_adam_out": ([gp, i64, vp, vp, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

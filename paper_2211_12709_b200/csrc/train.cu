@@ -94,7 +94,7 @@ template <>
 __device__ __forceinline__ double sqrt_rn<double>(double a) { return __dsqrt_rn(a); }
 
 template <typename R>
-__global__ void __launch_bounds__(kTT) k_adam(long long n, R* __restrict__ p, const R* __restrict__ g,
+__global__ void __launch_bounds__(kTT) k_adam(long long n, const R* pin, R* p, const R* __restrict__ g,
                                               R* __restrict__ m, R* __restrict__ v, R lr, R b1, R one_m_b1, R b2,
                                               R one_m_b2, R c1, R c2, R eps) {
   for (long long i = (long long)blockIdx.x * kTT + threadIdx.x; i < n; i += (long long)gridDim.x * kTT) {
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kTT) k_adam(long long n, R* __restrict__ p, co
     const R m_hat = div_rn(mi, c1);
     const R v_hat = div_rn(vi, c2);
     const R upd = div_rn(mul_rn(lr, m_hat), add_rn(sqrt_rn(v_hat), eps));
-    p[i] = add_rn(p[i], -upd);                     // p -= lr * m_hat / (sqrt(v_hat) + eps)
+    p[i] = add_rn(pin[i], -upd);                   // p -= lr * m_hat / (sqrt(v_hat) + eps)
     m[i] = mi;
     v[i] = vi;
   }
@@ -126,13 +126,15 @@ __device__ __forceinline__ void adam1(float& p, float gi, float& m, float& v, fl
   v = vi;
 }
 
-__global__ void __launch_bounds__(kTT) k_adam4(long long n4, float4* __restrict__ p, const float4* __restrict__ g,
+// pin may alias p (in place) or not (the updated parameter written to a fresh
+// buffer: no copy pass before the update)
+__global__ void __launch_bounds__(kTT) k_adam4(long long n4, const float4* pin, float4* p, const float4* __restrict__ g,
                                                float4* __restrict__ m, float4* __restrict__ v, float lr, float b1,
                                                float one_m_b1, float b2, float one_m_b2, float c1, float c2,
                                                float eps) {
   for (long long i = (long long)blockIdx.x * kTT + threadIdx.x; i < n4; i += (long long)gridDim.x * kTT) {
     const float4 gi = __ldcs(g + i);
-    float4 pi = __ldcs(p + i), mi = __ldcs(m + i), vi = __ldcs(v + i);
+    float4 pi = __ldcs(pin + i), mi = __ldcs(m + i), vi = __ldcs(v + i);
     adam1(pi.x, gi.x, mi.x, vi.x, lr, b1, one_m_b1, b2, one_m_b2, c1, c2, eps);
     adam1(pi.y, gi.y, mi.y, vi.y, lr, b1, one_m_b1, b2, one_m_b2, c1, c2, eps);
     adam1(pi.z, gi.z, mi.z, vi.z, lr, b1, one_m_b1, b2, one_m_b2, c1, c2, eps);
@@ -174,9 +176,10 @@ extern "C" int dfno_mse_grad(const dfno_geom* g, int64_t n, const void* pred, co
   return DFNO_OK;
 }
 
-extern "C" int dfno_adam(const dfno_geom* g, int64_t n, void* param, const void* grad, void* m, void* v, double lr,
-                         double beta1, double beta2, double eps, int step, void* stream) {
-  if (!g || !param || !grad || !m || !v) return DFNO_ERR_NULL;
+namespace {
+int adam_launch(const dfno_geom* g, int64_t n, const void* pin, void* param, const void* grad, void* m, void* v,
+                double lr, double beta1, double beta2, double eps, int step, void* stream) {
+  if (!g || !pin || !param || !grad || !m || !v) return DFNO_ERR_NULL;
   if (n < 0 || step < 1) return DFNO_ERR_DIMENSION;
   if (n == 0) return DFNO_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -187,23 +190,36 @@ extern "C" int dfno_adam(const dfno_geom* g, int64_t n, void* param, const void*
   // the array dtype at each binary op (d/training.py:66-73)
   const double c1 = 1.0 - pow(beta1, step), c2 = 1.0 - pow(beta2, step);
   const bool vec4 = g->dtype == DFNO_F32 && n % 4 == 0 &&
-                    (((uintptr_t)param | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) == 0;
+                    (((uintptr_t)pin | (uintptr_t)param | (uintptr_t)grad | (uintptr_t)m | (uintptr_t)v) & 15) == 0;
   if (vec4) {
     long long b4 = (n / 4 + kTT - 1) / kTT;
     if (b4 > cap) b4 = cap;
-    k_adam4<<<(unsigned)b4, kTT, 0, st>>>(n / 4, (float4*)param, (const float4*)grad, (float4*)m, (float4*)v,
-                                          (float)lr, (float)beta1, (float)(1.0 - beta1), (float)beta2,
-                                          (float)(1.0 - beta2), (float)c1, (float)c2, (float)eps);
+    k_adam4<<<(unsigned)b4, kTT, 0, st>>>(n / 4, (const float4*)pin, (float4*)param, (const float4*)grad,
+                                          (float4*)m, (float4*)v, (float)lr, (float)beta1, (float)(1.0 - beta1),
+                                          (float)beta2, (float)(1.0 - beta2), (float)c1, (float)c2, (float)eps);
   } else if (g->dtype == DFNO_F32)
-    k_adam<float><<<(unsigned)blocks, kTT, 0, st>>>(n, (float*)param, (const float*)grad, (float*)m, (float*)v,
-                                                    (float)lr, (float)beta1, (float)(1.0 - beta1), (float)beta2,
-                                                    (float)(1.0 - beta2), (float)c1, (float)c2, (float)eps);
+    k_adam<float><<<(unsigned)blocks, kTT, 0, st>>>(n, (const float*)pin, (float*)param, (const float*)grad,
+                                                    (float*)m, (float*)v, (float)lr, (float)beta1,
+                                                    (float)(1.0 - beta1), (float)beta2, (float)(1.0 - beta2),
+                                                    (float)c1, (float)c2, (float)eps);
   else if (g->dtype == DFNO_F64)
-    k_adam<double><<<(unsigned)blocks, kTT, 0, st>>>(n, (double*)param, (const double*)grad, (double*)m,
-                                                     (double*)v, lr, beta1, 1.0 - beta1, beta2, 1.0 - beta2, c1, c2,
-                                                     eps);
+    k_adam<double><<<(unsigned)blocks, kTT, 0, st>>>(n, (const double*)pin, (double*)param, (const double*)grad,
+                                                     (double*)m, (double*)v, lr, beta1, 1.0 - beta1, beta2,
+                                                     1.0 - beta2, c1, c2, eps);
   else
     return DFNO_ERR_DTYPE;
   DFNO_CUDA_CHECK_LAUNCH();
   return DFNO_OK;
+}
+}  // namespace
+
+extern "C" int dfno_adam(const dfno_geom* g, int64_t n, void* param, const void* grad, void* m, void* v, double lr,
+                         double beta1, double beta2, double eps, int step, void* stream) {
+  return adam_launch(g, n, param, param, grad, m, v, lr, beta1, beta2, eps, step, stream);
+}
+
+extern "C" int dfno_adam_out(const dfno_geom* g, int64_t n, const void* param, void* param_out, const void* grad,
+                             void* m, void* v, double lr, double beta1, double beta2, double eps, int step,
+                             void* stream) {
+  return adam_launch(g, n, param, param_out, grad, m, v, lr, beta1, beta2, eps, step, stream);
 }

@@ -9,7 +9,7 @@ bit-identical each step; the spectral weights update their ky shard locally.
 
 Device work is three libdfno kernels per step besides the forward /
 backward: the fused residual + loss + output-gradient pass (dfno_mse_grad),
-and Adam on each parameter's real view (dfno_adam) with the reference's fp32
+and Adam on each parameter's real view (dfno_adam_out, written to a new array) with the reference's fp32
 operation order.  Only the scalar loss crosses to the host.
 """
 
@@ -63,18 +63,20 @@ def adam_update(state: AdamState, key: str, param: DenseTensor, grad: DenseTenso
     if not _lib.available():
         raise _lib.ExtensionMissingError("libdfno.so and a CUDA device are required (no CPU fallback)")
     lib = _lib.load()
-    p = param.data.to("cuda", copy=True).contiguous() if not param.data.is_cuda else param.data.clone()
+    p_in = param.data.to("cuda").contiguous()
+    p = torch.empty_like(p_in)  # the new parameter (the old one stays valid, as the reference's arrays do)
     gd = grad.data.to(p.device).contiguous()
     if gd.dtype != p.dtype or gd.shape != p.shape:
         raise ShapeMismatchError(f"{key}: gradient {tuple(gd.shape)} {gd.dtype} vs parameter {tuple(p.shape)} {p.dtype}")
-    pv, gv = _real_view(p), _real_view(gd)
+    pin_v, pv, gv = _real_view(p_in), _real_view(p), _real_view(gd)
     if key not in state.m:
         state.m[key] = torch.zeros_like(pv)
         state.v[key] = torch.zeros_like(pv)
     g = _geom_for(p.dtype)
-    _lib.check(lib.dfno_adam(ctypes.byref(g), pv.numel(), _lib.ptr(pv), _lib.ptr(gv), _lib.ptr(state.m[key]),
-                             _lib.ptr(state.v[key]), float(lr), float(state.beta1), float(state.beta2),
-                             float(state.eps), int(state.step), _lib.stream_handle()), "dfno_adam")
+    _lib.check(lib.dfno_adam_out(ctypes.byref(g), pv.numel(), _lib.ptr(pin_v), _lib.ptr(pv), _lib.ptr(gv),
+                                 _lib.ptr(state.m[key]), _lib.ptr(state.v[key]), float(lr), float(state.beta1),
+                                 float(state.beta2), float(state.eps), int(state.step), _lib.stream_handle()),
+               "dfno_adam_out")
     return DenseTensor(param.labels, p)
 
 
